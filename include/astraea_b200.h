@@ -1,0 +1,211 @@
+/*
+ * astraea_b200.h -- C ABI of the B200 (sm_100a) data path driven by
+ * Astraea's state-aware scheduler (arXiv 2512.14142).
+ *
+ * The reference (pkg/src/agentsched, pure Python) has no FFI: every GPU
+ * action is a cost-model delay. Each entry point below names the reference
+ * symbol whose *delay* it replaces with real device work; the host plugin
+ * (paper_2512_14142_b200.gpu, and the ctypes stub in INTEGRATION.md) calls
+ * them at exactly those seams.
+ *
+ * Conventions
+ *   - Every function returns int: 0 on success, a positive cudaError_t, or
+ *     a negative ASTRAEA_E* code. Nothing throws across the ABI.
+ *   - Pointers named *_dev are device (HBM) pointers; *_host are host
+ *     pointers (pinned where a copy engine or SM reads them directly).
+ *   - All device work is stream-ordered on the caller's stream (a
+ *     cudaStream_t passed as void*); no call synchronises the device except
+ *     where stated.
+ *   - bf16 tensors are row-major and contiguous unless a stride is given.
+ *
+ * KV pool layout (HBM), block-major so a swap moves whole blocks:
+ *   pool[num_blocks][num_layers][2 (K,V)][num_kv_heads][block_tokens][head_dim]  bf16
+ * One (block, layer, K|V, head) page is block_tokens*head_dim*2 bytes and
+ * contiguous (4 KiB for head_dim 128): the unit the decode kernel stages
+ * into shared memory with one cp.async.bulk.
+ *
+ * Host swap slot layout (pinned), token-compact, exactly
+ * n_tokens * kv_bytes_per_token bytes:
+ *   slot[num_layers][2][num_kv_heads][n_tokens][head_dim]  bf16
+ */
+#ifndef ASTRAEA_B200_H
+#define ASTRAEA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define ASTRAEA_API __attribute__((visibility("default")))
+#else
+#define ASTRAEA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  ASTRAEA_OK = 0,
+  ASTRAEA_EINVAL = -1,      /* bad argument / shape */
+  ASTRAEA_ENOBLOCKS = -2,   /* allocator cannot satisfy the request (nothing taken) */
+  ASTRAEA_EDOUBLEFREE = -3, /* block returned twice or out of range */
+  ASTRAEA_EUNSUPPORTED = -4 /* shape/dtype combination not compiled in */
+};
+
+ASTRAEA_API const char* astraea_status_string(int status);
+ASTRAEA_API int astraea_abi_version(void);
+
+typedef struct {
+  int32_t num_layers;
+  int32_t num_kv_heads;
+  int32_t head_dim;      /* 64 or 128 */
+  int32_t block_tokens;  /* 16 */
+  int32_t num_blocks;
+} astraea_kv_geometry;
+
+/* Bytes of one pool block (all layers, K and V). */
+ASTRAEA_API size_t astraea_kv_block_bytes(const astraea_kv_geometry* g);
+/* Bytes per token of KV: the reference's MemoryModel.bytes_per_token
+ * (kvcache.py:87-99) made concrete. */
+ASTRAEA_API size_t astraea_kv_bytes_per_token(const astraea_kv_geometry* g);
+
+/* ---- block allocator (host free list over [0, num_blocks)) --------------
+ * Mirrors MemoryModel.allocate / release (kvcache.py:118-134) at block
+ * granularity. LIFO reuse keeps recently freed (L2-warm) blocks hot. */
+typedef struct astraea_block_allocator astraea_block_allocator;
+ASTRAEA_API int astraea_alloc_create(int32_t num_blocks, astraea_block_allocator** out);
+ASTRAEA_API int astraea_alloc_destroy(astraea_block_allocator* a);
+/* Take n blocks into out_ids_host; ASTRAEA_ENOBLOCKS (and nothing taken) if short. */
+ASTRAEA_API int astraea_alloc_take(astraea_block_allocator* a, int32_t n, int32_t* out_ids_host);
+/* Return blocks; ASTRAEA_EDOUBLEFREE if any id is free already or out of range
+ * (in which case nothing is returned). */
+ASTRAEA_API int astraea_alloc_give(astraea_block_allocator* a, const int32_t* ids_host, int32_t n);
+ASTRAEA_API int32_t astraea_alloc_free_count(const astraea_block_allocator* a);
+
+/* ---- K1 / K2: KV swap ----------------------------------------------------------
+ * Replace the swap delay kv_tokens / swap_bandwidth (kvcache.py:136-137)
+ * scheduled at simulator.py:239-245 (out) and simulator.py:299-325 (in),
+ * completed by KvCacheManager.complete_swap_out / complete_swap_in
+ * (kvcache.py:230-258).
+ * block_ids_host lists the request's blocks in context order; only the first
+ * n_tokens tokens are moved (the last block's padding is not).
+ * mode 0: SM gather/scatter kernel writing/reading the pinned slot through
+ *         its mapped device address (zero-copy over the host link);
+ * mode 1: copy engines, one strided 2-D DMA per block.
+ * host slot must be pinned (cudaHostAlloc / cudaHostRegister). */
+enum { ASTRAEA_SWAP_KERNEL = 0, ASTRAEA_SWAP_DMA = 1 };
+ASTRAEA_API int astraea_kv_swap_out(const astraea_kv_geometry* g, const void* pool_dev,
+                        const int32_t* block_ids_host, int32_t n_blocks, int32_t n_tokens,
+                        void* slot_host, int mode, void* stream);
+ASTRAEA_API int astraea_kv_swap_in(const astraea_kv_geometry* g, void* pool_dev,
+                       const int32_t* block_ids_host, int32_t n_blocks, int32_t n_tokens,
+                       const void* slot_host, int mode, void* stream);
+/* Device-to-device block copy (pool compaction / defragmentation). */
+ASTRAEA_API int astraea_kv_copy_blocks(const astraea_kv_geometry* g, void* pool_dev,
+                           const int32_t* src_ids_host, const int32_t* dst_ids_host,
+                           int32_t n, void* stream);
+
+/* ---- K3: block table build / compaction ------------------------------------------
+ * Replaces the implicit per-request residency of kvcache.py:219-222,
+ * 260-292 with the dense table the attention kernels read.
+ * csr_ptr_dev[R+1], csr_ids_dev[...]: every request's block list.
+ * rows_dev[B]: which CSR rows form the batch (retired members are simply
+ * left out -> compaction). Writes table_dev[B][max_blocks] (pad -1) and
+ * ctx_dev[B] = ctx_src_dev[rows[b]]. */
+ASTRAEA_API int astraea_block_table_build(const int32_t* csr_ptr_dev, const int32_t* csr_ids_dev,
+                              const int32_t* rows_dev, const int32_t* ctx_src_dev, int32_t B,
+                              int32_t max_blocks, int32_t* table_dev, int32_t* ctx_dev,
+                              void* stream);
+
+/* ---- decode-loop driver (device side, CUDA-graph capturable) ----------------------------
+ * Advances the batch by one decode step without host involvement, so the
+ * whole step (advance + layers + sampling) is one replayable graph.
+ * step = *step_dev (then *step_dev += 1). For row b with step < n_gen[b]:
+ *   fed token  = step == 0 ? first_tok[b] : sampled[b]
+ *   position   = base_pos[b] + step;  ctx[b] = position + 1
+ *   slot       = table[b][position / block_tokens] * block_tokens + position % block_tokens
+ *   hist[b * hist_stride + step] = fed token
+ * and at step == n_gen[b]: hist[b * hist_stride + n_gen[b]] = sampled[b] (the
+ * row's pending next token), so hist rows need n_gen[b] + 1 entries.
+ * Rows with step >= n_gen[b] are retired: slot -1, ctx 0 (attention and
+ * append skip them) -- the compaction the reference's parallel-max batch
+ * implies when members finish at their own n_gen (simulator.py:96-98). */
+ASTRAEA_API int astraea_decode_advance(int32_t* step_dev, int32_t B, const int32_t* n_gen_dev,
+                           const int32_t* base_pos_dev, const int32_t* first_tok_dev,
+                           const int32_t* sampled_dev, const int32_t* table_dev,
+                           int32_t max_blocks, int32_t block_tokens, int32_t* tokens_dev,
+                           int32_t* positions_dev, int32_t* slots_dev, int32_t* ctx_dev,
+                           int32_t* hist_dev, int32_t hist_stride, void* stream);
+
+/* ---- K5: RoPE + KV append ------------------------------------------------------------
+ * Materialises state.kv_tokens = context_after(...) (simulator.py:367-369)
+ * as real K/V rows. qkv_dev[T][(Hq + 2*Hkv) * D] is the fused projection
+ * output; RoPE (theta, NeoX half-split) is applied to q (in place) and k;
+ * k and v are written to pool slot slots_dev[t] = block * block_tokens + offset
+ * (slot < 0: row skipped). positions_dev[T] are absolute token positions. */
+ASTRAEA_API int astraea_rope_kv_append(const astraea_kv_geometry* g, void* pool_dev, int32_t layer,
+                           void* qkv_dev, int32_t T, int32_t num_q_heads,
+                           const int32_t* positions_dev, const int32_t* slots_dev,
+                           float rope_theta, void* stream);
+
+/* ---- K4: paged decode attention ------------------------------------------------------------
+ * Replaces n_gen * seconds_per_token (simulator.py:337) -- one decode step
+ * of the scheduler's mixed batch. q_dev: row b at q_dev + b*q_row_stride elements
+ * holds [Hq][D] (so q can be read in place from the fused QKV rows);
+ * table_dev[B][max_blocks];
+ * ctx_dev[B] = tokens visible to the row (0 -> output zeros). out_dev[B][Hq][D].
+ * workspace: float buffer, astraea_decode_workspace_bytes(...) bytes. */
+ASTRAEA_API size_t astraea_decode_workspace_bytes(int32_t B, int32_t num_q_heads, int32_t head_dim,
+                                      int32_t max_blocks);
+ASTRAEA_API int astraea_paged_decode_attention(const astraea_kv_geometry* g, const void* pool_dev,
+                                   int32_t layer, const void* q_dev, int32_t q_row_stride,
+                                   int32_t B, int32_t num_q_heads, const int32_t* table_dev,
+                                   int32_t max_blocks, const int32_t* ctx_dev, float scale,
+                                   void* out_dev, void* workspace_dev, size_t workspace_bytes,
+                                   void* stream);
+
+/* ---- K7: paged prefill attention (causal, varlen) ---------------------------------------------
+ * Replaces prefill_seconds(n_in + extra) (simulator.py:335-336): the
+ * appended API result, or the whole context after a discard.
+ * q_dev rows of [Hq][D] at stride q_row_stride (T = cu_q[S] rows); out_dev is
+ * dense [T][Hq][D]; sequence s owns q rows [cu_q[s], cu_q[s+1])
+ * whose absolute positions are ctx[s]-len_s .. ctx[s]-1 and attends causally
+ * to its paged context table[s][*] of ctx[s] tokens. */
+ASTRAEA_API int astraea_paged_prefill_attention(const astraea_kv_geometry* g, const void* pool_dev,
+                                    int32_t layer, const void* q_dev, int32_t q_row_stride,
+                                    const int32_t* cu_q_dev,
+                                    int32_t S, int32_t max_q_len, int32_t num_q_heads,
+                                    const int32_t* table_dev, int32_t max_blocks,
+                                    const int32_t* ctx_dev, float scale, void* out_dev,
+                                    void* stream);
+
+/* ---- K6 / K9: dense projections on tcgen05 ------------------------------------------------------
+ * C[M][N] = A[M][K] . W[N][K]^T (+ residual[M][N]), bf16 in, fp32 TMEM
+ * accumulate, bf16 out. lda/ldw/ldc in elements. Prefill (M large) and decode
+ * (M = batch) both run on tcgen05.mma; decode uses the swapped-operand form
+ * (W rows on the MMA M axis) with split-K. workspace may be NULL when
+ * astraea_gemm_workspace_bytes() returns 0. */
+enum { ASTRAEA_EPI_NONE = 0, ASTRAEA_EPI_RESIDUAL = 1 };
+ASTRAEA_API size_t astraea_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K);
+ASTRAEA_API int astraea_gemm_bf16(const void* A_dev, int32_t lda, const void* W_dev, int32_t ldw,
+                      void* C_dev, int32_t ldc, int32_t M, int32_t N, int32_t K,
+                      const void* residual_dev, int32_t epilogue, void* workspace_dev,
+                      size_t workspace_bytes, void* stream);
+
+/* ---- K8: small fused ops --------------------------------------------------------------------------- */
+/* y = rmsnorm(x + r) * w ; if resid_out_dev != NULL it receives x + r. r may be NULL. */
+ASTRAEA_API int astraea_rmsnorm(const void* x_dev, const void* r_dev, const void* w_dev, void* y_dev,
+                    void* resid_out_dev, int32_t rows, int32_t dim, float eps, void* stream);
+/* out[T][F] = silu(gu[T][0:F]) * gu[T][F:2F] */
+ASTRAEA_API int astraea_silu_mul(const void* gu_dev, void* out_dev, int32_t T, int32_t F, void* stream);
+/* out[T][dim] = table[ids[T]][dim] */
+ASTRAEA_API int astraea_embedding(const int32_t* ids_dev, const void* table_dev, void* out_dev, int32_t T,
+                      int32_t dim, void* stream);
+/* ids_out[r] = argmax_j logits[r][j] (lowest index on ties); logits bf16 [rows][vocab]. */
+ASTRAEA_API int astraea_argmax(const void* logits_dev, int32_t rows, int32_t vocab, int32_t* ids_out_dev,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ASTRAEA_B200_H */

@@ -1,0 +1,130 @@
+"""ctypes binding of ``libastraea_b200.so`` (C ABI: include/astraea_b200.h).
+
+This is the only place Python touches the native library. There is no CPU
+fallback: if the library is missing or no CUDA device is present, every
+device entry point raises, loudly. Torch is used for device memory, pinned
+host memory and streams only; the arithmetic happens in the sm_100a
+kernels behind these calls.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from ..host.errors import DeviceError
+
+LIB_PATH = Path(__file__).resolve().parent.parent / "lib" / "libastraea_b200.so"
+
+SWAP_KERNEL = 0
+SWAP_DMA = 1
+EPI_NONE = 0
+EPI_RESIDUAL = 1
+
+
+class KvGeometry(ctypes.Structure):
+    _fields_ = [
+        ("num_layers", ctypes.c_int32),
+        ("num_kv_heads", ctypes.c_int32),
+        ("head_dim", ctypes.c_int32),
+        ("block_tokens", ctypes.c_int32),
+        ("num_blocks", ctypes.c_int32),
+    ]
+
+
+_i32 = ctypes.c_int32
+_vp = ctypes.c_void_p
+_sz = ctypes.c_size_t
+_f32 = ctypes.c_float
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_geo = ctypes.POINTER(KvGeometry)
+
+# name -> (restype, argtypes); must match include/astraea_b200.h exactly.
+SIGNATURES = {
+    "astraea_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "astraea_abi_version": (ctypes.c_int, []),
+    "astraea_kv_block_bytes": (_sz, [_geo]),
+    "astraea_kv_bytes_per_token": (_sz, [_geo]),
+    "astraea_alloc_create": (ctypes.c_int, [_i32, ctypes.POINTER(_vp)]),
+    "astraea_alloc_destroy": (ctypes.c_int, [_vp]),
+    "astraea_alloc_take": (ctypes.c_int, [_vp, _i32, _i32p]),
+    "astraea_alloc_give": (ctypes.c_int, [_vp, _i32p, _i32]),
+    "astraea_alloc_free_count": (_i32, [_vp]),
+    "astraea_kv_swap_out": (ctypes.c_int, [_geo, _vp, _i32p, _i32, _i32, _vp, ctypes.c_int, _vp]),
+    "astraea_kv_swap_in": (ctypes.c_int, [_geo, _vp, _i32p, _i32, _i32, _vp, ctypes.c_int, _vp]),
+    "astraea_kv_copy_blocks": (ctypes.c_int, [_geo, _vp, _i32p, _i32p, _i32, _vp]),
+    "astraea_block_table_build": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp]),
+    "astraea_rope_kv_append": (ctypes.c_int, [_geo, _vp, _i32, _vp, _i32, _i32, _vp, _vp, _f32, _vp]),
+    "astraea_decode_workspace_bytes": (_sz, [_i32, _i32, _i32, _i32]),
+    "astraea_paged_decode_attention": (
+        ctypes.c_int, [_geo, _vp, _i32, _vp, _i32, _i32, _i32, _vp, _i32, _vp, _f32, _vp, _vp, _sz, _vp]),
+    "astraea_paged_prefill_attention": (
+        ctypes.c_int, [_geo, _vp, _i32, _vp, _i32, _vp, _i32, _i32, _i32, _vp, _i32, _vp, _f32, _vp, _vp]),
+    "astraea_gemm_workspace_bytes": (_sz, [_i32, _i32, _i32]),
+    "astraea_gemm_bf16": (
+        ctypes.c_int, [_vp, _i32, _vp, _i32, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _sz, _vp]),
+    "astraea_decode_advance": (
+        ctypes.c_int, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp]),
+    "astraea_rmsnorm": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _f32, _vp]),
+    "astraea_silu_mul": (ctypes.c_int, [_vp, _vp, _i32, _i32, _vp]),
+    "astraea_embedding": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i32, _vp]),
+    "astraea_argmax": (ctypes.c_int, [_vp, _i32, _i32, _vp, _vp]),
+}
+
+_LIB = None
+
+
+def load(path: os.PathLike | None = None):
+    """Load and type the library (no device needed)."""
+    global _LIB
+    if _LIB is not None and path is None:
+        return _LIB
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise DeviceError(
+            f"{p} not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(nvcc, sm_100a). There is no CPU fallback."
+        )
+    lib = ctypes.CDLL(str(p))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _LIB = lib
+    return lib
+
+
+def check(status: int, what: str) -> None:
+    if status != 0:
+        msg = load().astraea_status_string(status).decode()
+        raise DeviceError(f"{what} failed with status {status}: {msg}")
+
+
+def require_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: the B200 data path has no CPU fallback")
+    major, minor = torch.cuda.get_device_capability()
+    if major != 10:
+        raise DeviceError(f"need an sm_100 (B200) device, found sm_{major}{minor}")
+    return load()
+
+
+def ptr(t) -> int:
+    """Device (or pinned host) address of a torch tensor, None -> 0."""
+    return 0 if t is None else t.data_ptr()
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def i32_array(values) -> ctypes.Array:
+    arr = (ctypes.c_int32 * len(values))(*values)
+    return arr

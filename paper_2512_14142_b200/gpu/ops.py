@@ -1,0 +1,185 @@
+"""Tensor-level wrappers over the C ABI (shape checks + pointer passing).
+
+Every function launches exactly the sm_100a kernels named in
+include/astraea_b200.h on the current torch stream (or the given one) and
+returns without synchronising. Inputs must already live on the device.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import lib as L
+
+
+def _s(stream):
+    return L.stream_handle(stream)
+
+
+def geometry(num_layers, num_kv_heads, head_dim, num_blocks, block_tokens=16) -> L.KvGeometry:
+    return L.KvGeometry(num_layers, num_kv_heads, head_dim, block_tokens, num_blocks)
+
+
+def gemm(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None,
+         residual: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+         stream=None) -> torch.Tensor:
+    """out[M,N] = a[M,K] @ w[N,K]^T (+ residual), tcgen05 tensor cores."""
+    lib = L.require_cuda()
+    M, K = a.shape
+    N = w.shape[0]
+    assert w.shape[1] == K and a.dtype == torch.bfloat16 and w.dtype == torch.bfloat16
+    assert a.stride(1) == 1 and w.stride(1) == 1
+    if out is None:
+        out = torch.empty(M, N, dtype=torch.bfloat16, device=a.device)
+    need = lib.astraea_gemm_workspace_bytes(M, N, K)
+    if need and (workspace is None or workspace.numel() * workspace.element_size() < need):
+        workspace = torch.zeros(need // 4 + 1, dtype=torch.float32, device=a.device)
+    L.check(lib.astraea_gemm_bf16(
+        L.ptr(a), a.stride(0), L.ptr(w), w.stride(0), L.ptr(out), out.stride(0), M, N, K,
+        L.ptr(residual), L.EPI_RESIDUAL if residual is not None else L.EPI_NONE,
+        L.ptr(workspace), 0 if workspace is None else workspace.numel() * workspace.element_size(),
+        _s(stream)), "gemm_bf16")
+    return out
+
+
+def rmsnorm(x, weight, eps, out=None, residual=None, resid_out=None, stream=None):
+    lib = L.require_cuda()
+    rows, dim = x.shape
+    if out is None:
+        out = torch.empty_like(x)
+    L.check(lib.astraea_rmsnorm(L.ptr(x), L.ptr(residual), L.ptr(weight), L.ptr(out), L.ptr(resid_out),
+                                rows, dim, eps, _s(stream)), "rmsnorm")
+    return out
+
+
+def silu_mul(gu, out=None, stream=None):
+    lib = L.require_cuda()
+    T, F2 = gu.shape
+    F = F2 // 2
+    if out is None:
+        out = torch.empty(T, F, dtype=gu.dtype, device=gu.device)
+    L.check(lib.astraea_silu_mul(L.ptr(gu), L.ptr(out), T, F, _s(stream)), "silu_mul")
+    return out
+
+
+def embedding(ids, table, out=None, stream=None):
+    lib = L.require_cuda()
+    T = ids.shape[0]
+    dim = table.shape[1]
+    if out is None:
+        out = torch.empty(T, dim, dtype=table.dtype, device=table.device)
+    L.check(lib.astraea_embedding(L.ptr(ids), L.ptr(table), L.ptr(out), T, dim, _s(stream)), "embedding")
+    return out
+
+
+def argmax(logits, out=None, stream=None):
+    lib = L.require_cuda()
+    rows, vocab = logits.shape
+    if out is None:
+        out = torch.empty(rows, dtype=torch.int32, device=logits.device)
+    L.check(lib.astraea_argmax(L.ptr(logits), rows, vocab, L.ptr(out), _s(stream)), "argmax")
+    return out
+
+
+def rope_kv_append(geo, pool, layer, qkv, num_q_heads, positions, slots, theta, stream=None):
+    lib = L.require_cuda()
+    L.check(lib.astraea_rope_kv_append(ctypes.byref(geo), L.ptr(pool), layer, L.ptr(qkv), qkv.shape[0],
+                                       num_q_heads, L.ptr(positions), L.ptr(slots), theta, _s(stream)),
+            "rope_kv_append")
+
+
+def decode_attention(geo, pool, layer, q, q_row_stride, B, num_q_heads, table, ctx, scale, out,
+                     workspace, stream=None):
+    lib = L.require_cuda()
+    L.check(lib.astraea_paged_decode_attention(
+        ctypes.byref(geo), L.ptr(pool), layer, L.ptr(q), q_row_stride, B, num_q_heads, L.ptr(table),
+        table.shape[1], L.ptr(ctx), scale, L.ptr(out), L.ptr(workspace),
+        workspace.numel() * workspace.element_size(), _s(stream)), "paged_decode_attention")
+    return out
+
+
+def decode_workspace(B, num_q_heads, head_dim, max_blocks, device) -> torch.Tensor:
+    lib = L.load()
+    n = lib.astraea_decode_workspace_bytes(B, num_q_heads, head_dim, max_blocks)
+    return torch.empty(n // 4 + 1, dtype=torch.float32, device=device)
+
+
+def prefill_attention(geo, pool, layer, q, q_row_stride, cu_q, S, max_q_len, num_q_heads, table, ctx,
+                      scale, out, stream=None):
+    lib = L.require_cuda()
+    L.check(lib.astraea_paged_prefill_attention(
+        ctypes.byref(geo), L.ptr(pool), layer, L.ptr(q), q_row_stride, L.ptr(cu_q), S, max_q_len,
+        num_q_heads, L.ptr(table), table.shape[1], L.ptr(ctx), scale, L.ptr(out), _s(stream)),
+        "paged_prefill_attention")
+    return out
+
+
+def block_table_build(csr_ptr, csr_ids, rows, ctx_src, max_blocks, table, ctx, stream=None):
+    lib = L.require_cuda()
+    L.check(lib.astraea_block_table_build(L.ptr(csr_ptr), L.ptr(csr_ids), L.ptr(rows), L.ptr(ctx_src),
+                                          rows.shape[0], max_blocks, L.ptr(table), L.ptr(ctx), _s(stream)),
+            "block_table_build")
+
+
+def decode_advance(step, B, n_gen, base_pos, first_tok, sampled, table, block_tokens, tokens, positions,
+                   slots, ctx, hist=None, hist_stride=0, stream=None):
+    lib = L.require_cuda()
+    L.check(lib.astraea_decode_advance(
+        L.ptr(step), B, L.ptr(n_gen), L.ptr(base_pos), L.ptr(first_tok), L.ptr(sampled), L.ptr(table),
+        table.shape[1], block_tokens, L.ptr(tokens), L.ptr(positions), L.ptr(slots), L.ptr(ctx),
+        L.ptr(hist), hist_stride, _s(stream)), "decode_advance")
+
+
+def swap_out(geo, pool, block_ids, n_tokens, slot, mode=L.SWAP_KERNEL, stream=None):
+    lib = L.require_cuda()
+    ids = L.i32_array(block_ids)
+    L.check(lib.astraea_kv_swap_out(ctypes.byref(geo), L.ptr(pool), ids, len(block_ids), n_tokens,
+                                    L.ptr(slot), mode, _s(stream)), "kv_swap_out")
+
+
+def swap_in(geo, pool, block_ids, n_tokens, slot, mode=L.SWAP_KERNEL, stream=None):
+    lib = L.require_cuda()
+    ids = L.i32_array(block_ids)
+    L.check(lib.astraea_kv_swap_in(ctypes.byref(geo), L.ptr(pool), ids, len(block_ids), n_tokens,
+                                   L.ptr(slot), mode, _s(stream)), "kv_swap_in")
+
+
+def copy_blocks(geo, pool, src_ids, dst_ids, stream=None):
+    lib = L.require_cuda()
+    L.check(lib.astraea_kv_copy_blocks(ctypes.byref(geo), L.ptr(pool), L.i32_array(src_ids),
+                                       L.i32_array(dst_ids), len(src_ids), _s(stream)), "kv_copy_blocks")
+
+
+class BlockAllocator:
+    """Host free list over the pool's blocks (native, LIFO)."""
+
+    def __init__(self, num_blocks: int):
+        self._lib = L.load()
+        h = ctypes.c_void_p()
+        L.check(self._lib.astraea_alloc_create(num_blocks, ctypes.byref(h)), "alloc_create")
+        self._h = h
+        self.num_blocks = num_blocks
+
+    def take(self, n: int) -> list[int]:
+        if n == 0:
+            return []
+        buf = (ctypes.c_int32 * n)()
+        L.check(self._lib.astraea_alloc_take(self._h, n, buf), f"alloc_take({n})")
+        return list(buf)
+
+    def give(self, ids) -> None:
+        if not ids:
+            return
+        L.check(self._lib.astraea_alloc_give(self._h, L.i32_array(ids), len(ids)), "alloc_give")
+
+    @property
+    def free(self) -> int:
+        return self._lib.astraea_alloc_free_count(self._h)
+
+    def __del__(self):
+        try:
+            self._lib.astraea_alloc_destroy(self._h)
+        except Exception:
+            pass

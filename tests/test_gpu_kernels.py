@@ -1,0 +1,289 @@
+"""Kernel parity on a B200: every K1-K9 entry point through the C ABI
+against the CPU oracle (bit-exact for byte/index work, fp32 reference with
+a stated tolerance for floating point)."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import cuda_available
+from oracle import attention_ref, kvpool_ref
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not cuda_available(), reason="needs a B200")]
+
+from paper_2512_14142_b200.gpu import lib as L  # noqa: E402
+from paper_2512_14142_b200.gpu import ops  # noqa: E402
+
+DEV = "cuda"
+
+
+def rel_err(a, b):
+    a, b = a.float().cpu(), b.float().cpu()
+    return float((a - b).norm() / b.norm().clamp_min(1e-30))
+
+
+def make_pool(nb, Lyr, Hkv, D, seed=0):
+    g = torch.Generator(device=DEV).manual_seed(seed)
+    pool = torch.randn(nb * Lyr * 2 * Hkv * 16 * D, generator=g, device=DEV).bfloat16()
+    return pool, ops.geometry(Lyr, Hkv, D, nb)
+
+
+# ---------------------------------------------------------------- K1 / K2 swap
+
+@pytest.mark.parametrize("mode", [L.SWAP_KERNEL, L.SWAP_DMA])
+@pytest.mark.parametrize("Lyr,Hkv,D,n_tokens", [(4, 2, 64, 1), (4, 2, 64, 17), (4, 2, 64, 300),
+                                                (32, 8, 128, 1000), (80, 1, 128, 129)])
+def test_swap_out_matches_oracle_and_round_trips_bit_exact(mode, Lyr, Hkv, D, n_tokens):
+    nb_total = 96
+    pool, geo = make_pool(nb_total, Lyr, Hkv, D, seed=n_tokens)
+    nb = (n_tokens + 15) // 16
+    rng = np.random.default_rng(n_tokens)
+    src = rng.choice(nb_total, nb, replace=False).tolist()
+    bpt = Lyr * 2 * Hkv * D * 2
+    slot = torch.zeros(n_tokens * bpt, dtype=torch.uint8, pin_memory=True)
+    ops.swap_out(geo, pool, src, n_tokens, slot, mode)
+    torch.cuda.synchronize()
+    pool_np = pool.view(torch.int16).cpu().numpy().view(np.uint16)
+    want = kvpool_ref.swap_out_ref(pool_np, src, n_tokens, Lyr, Hkv, D)
+    got = slot.numpy().view(np.uint16).reshape(want.shape)
+    assert np.array_equal(got, want)
+    # scatter into different blocks, gather again: identical bytes
+    dst = [b for b in rng.permutation(nb_total).tolist() if b not in src][:nb]
+    before = pool.clone()
+    ops.swap_in(geo, pool, dst, n_tokens, slot, mode)
+    slot2 = torch.zeros_like(slot)
+    ops.swap_out(geo, pool, dst, n_tokens, slot2, mode)
+    torch.cuda.synchronize()
+    assert torch.equal(slot, slot2)
+    # swap-in wrote only the valid tokens of dst blocks
+    want_pool = kvpool_ref.swap_in_ref(before.view(torch.int16).cpu().numpy().view(np.uint16), dst,
+                                       n_tokens, want, Lyr, Hkv, D)
+    assert np.array_equal(pool.view(torch.int16).cpu().numpy().view(np.uint16), want_pool)
+
+
+def test_swap_rejects_bad_arguments():
+    pool, geo = make_pool(8, 2, 2, 64)
+    slot = torch.zeros(100 * 2 * 2 * 2 * 64 * 2, dtype=torch.uint8, pin_memory=True)
+    from paper_2512_14142_b200.host.errors import DeviceError
+    with pytest.raises(DeviceError):
+        ops.swap_out(geo, pool, [0, 1], 100, slot)          # 100 tokens need 7 blocks
+    with pytest.raises(DeviceError):
+        ops.swap_out(geo, pool, [0, 99], 20, slot)          # block id out of range
+
+
+def test_copy_blocks():
+    pool, geo = make_pool(16, 2, 2, 64)
+    ref = pool.clone().view(16, -1)
+    ops.copy_blocks(geo, pool, [1, 2], [7, 9])
+    torch.cuda.synchronize()
+    v = pool.view(16, -1)
+    assert torch.equal(v[7], ref[1]) and torch.equal(v[9], ref[2]) and torch.equal(v[0], ref[0])
+
+
+# ---------------------------------------------------------------- K3 table build
+
+def test_block_table_build_matches_oracle():
+    ptr = [0, 3, 3, 8, 9]
+    ids = [4, 5, 6, 10, 11, 12, 13, 14, 2]
+    rows = [3, 0, 2]
+    ctx_src = [40, 0, 70, 9]
+    d = lambda v: torch.tensor(v, dtype=torch.int32, device=DEV)  # noqa: E731
+    table = torch.empty(3, 6, dtype=torch.int32, device=DEV)
+    ctx = torch.empty(3, dtype=torch.int32, device=DEV)
+    ops.block_table_build(d(ptr), d(ids), d(rows), d(ctx_src), 6, table, ctx)
+    t, c = kvpool_ref.table_build_ref(ptr, ids, rows, ctx_src, 6)
+    assert table.cpu().numpy().tolist() == t.tolist()
+    assert ctx.cpu().numpy().tolist() == c.tolist()
+
+
+# ---------------------------------------------------------------- K5 rope + append
+
+@pytest.mark.parametrize("Hq,Hkv,D", [(8, 2, 64), (32, 8, 128)])
+def test_rope_kv_append(Hq, Hkv, D):
+    Lyr, nb, T = 3, 12, 37
+    pool, geo = make_pool(nb, Lyr, Hkv, D)
+    pool.zero_()
+    g = torch.Generator(device=DEV).manual_seed(3)
+    qkv = torch.randn(T, (Hq + 2 * Hkv) * D, generator=g, device=DEV).bfloat16()
+    orig = qkv.clone()
+    positions = torch.arange(100, 100 + T, dtype=torch.int32, device=DEV)
+    blocks = [9, 2, 5, 7, 11, 0, 1, 3, 4]
+    slots = [blocks[p // 16] * 16 + p % 16 for p in range(100, 100 + T)]
+    slots[5] = -1  # skipped row
+    ops.rope_kv_append(geo, pool, 1, qkv, Hq, positions, torch.tensor(slots, dtype=torch.int32, device=DEV),
+                       500000.0)
+    torch.cuda.synchronize()
+    q_ref = attention_ref.rope_ref(orig[:, : Hq * D].view(T, Hq, D).float().cpu(), positions.cpu(), 500000.0)
+    assert rel_err(qkv[:, : Hq * D].view(T, Hq, D), q_ref) < 4e-3
+    k_ref = attention_ref.rope_ref(orig[:, Hq * D:(Hq + Hkv) * D].view(T, Hkv, D).float().cpu(),
+                                   positions.cpu(), 500000.0)
+    v_ref = orig[:, (Hq + Hkv) * D:].view(T, Hkv, D).cpu()
+    p6 = pool.view(nb, Lyr, 2, Hkv, 16, D).cpu()
+    for t in range(T):
+        if slots[t] < 0:
+            continue
+        b, o = divmod(slots[t], 16)
+        assert torch.equal(p6[b, 1, 1, :, o], v_ref[t])
+        assert rel_err(p6[b, 1, 0, :, o], k_ref[t]) < 4e-3
+    b, o = divmod(blocks[(100 + 5) // 16] * 16 + (105 % 16), 16)
+    assert torch.count_nonzero(p6[b, 1, :, :, o]) == 0
+
+
+# ---------------------------------------------------------------- K4 decode attention
+
+@pytest.mark.parametrize("Hq,Hkv,D", [(32, 8, 128), (8, 2, 64), (8, 1, 128), (16, 2, 64)])
+@pytest.mark.parametrize("ctxs", [[1, 16, 17, 300], [2316, 5, 0, 1000, 64], [8000]])
+def test_decode_attention(Hq, Hkv, D, ctxs):
+    Lyr = 2
+    B = len(ctxs)
+    max_blocks = max(1, max((c + 15) // 16 for c in ctxs))
+    nb = B * max_blocks + 3
+    pool, geo = make_pool(nb, Lyr, Hkv, D, seed=B)
+    perm = torch.randperm(nb)[: B * max_blocks].view(B, max_blocks).int()
+    table = perm.clone()
+    for b, c in enumerate(ctxs):
+        table[b, (c + 15) // 16:] = -1
+    g = torch.Generator(device=DEV).manual_seed(7)
+    stride = (Hq + 2 * Hkv) * D
+    qkv = torch.randn(B, stride, generator=g, device=DEV).bfloat16()
+    out = torch.empty(B, Hq * D, dtype=torch.bfloat16, device=DEV)
+    ws = ops.decode_workspace(B, Hq, D, max_blocks, DEV)
+    scale = 1 / math.sqrt(D)
+    ctx_d = torch.tensor(ctxs, dtype=torch.int32, device=DEV)
+    ops.decode_attention(geo, pool, 1, qkv, stride, B, Hq, table.to(DEV), ctx_d, scale, out, ws)
+    torch.cuda.synchronize()
+    ref = attention_ref.decode_ref(pool.cpu(), 1, qkv[:, : Hq * D].view(B, Hq, D).cpu(), table, ctxs, scale,
+                                   Lyr, Hkv, D)
+    got = out.view(B, Hq, D).cpu().float()
+    for b, c in enumerate(ctxs):
+        if c == 0:
+            assert torch.count_nonzero(got[b]) == 0
+        else:
+            assert rel_err(got[b], ref[b]) < 1e-2, (b, c)
+
+
+# ---------------------------------------------------------------- K7 prefill attention
+
+@pytest.mark.parametrize("Hq,Hkv,D", [(32, 8, 128), (8, 2, 64)])
+@pytest.mark.parametrize("lens_ctx", [[(5, 5)], [(64, 64), (1, 300), (130, 1100)], [(700, 2316)]])
+def test_prefill_attention(Hq, Hkv, D, lens_ctx):
+    Lyr = 2
+    S = len(lens_ctx)
+    max_blocks = max((c + 15) // 16 for _, c in lens_ctx)
+    nb = S * max_blocks + 1
+    pool, geo = make_pool(nb, Lyr, Hkv, D, seed=S)
+    table = torch.randperm(nb)[: S * max_blocks].view(S, max_blocks).int()
+    cu = [0]
+    for n, _ in lens_ctx:
+        cu.append(cu[-1] + n)
+    T = cu[-1]
+    stride = (Hq + 2 * Hkv) * D
+    g = torch.Generator(device=DEV).manual_seed(11)
+    qkv = torch.randn(T, stride, generator=g, device=DEV).bfloat16()
+    out = torch.empty(T, Hq * D, dtype=torch.bfloat16, device=DEV)
+    ctx = [c for _, c in lens_ctx]
+    scale = 1 / math.sqrt(D)
+    ops.prefill_attention(geo, pool, 0, qkv, stride, torch.tensor(cu, dtype=torch.int32, device=DEV), S,
+                          max(n for n, _ in lens_ctx), Hq, table.to(DEV),
+                          torch.tensor(ctx, dtype=torch.int32, device=DEV), scale, out)
+    torch.cuda.synchronize()
+    ref = attention_ref.prefill_ref(pool.cpu(), 0, qkv[:, : Hq * D].view(T, Hq, D).cpu(), cu, table, ctx, scale,
+                                    Lyr, Hkv, D)
+    assert rel_err(out.view(T, Hq, D), ref) < 1e-2
+
+
+# ---------------------------------------------------------------- K6 / K9 GEMM (tcgen05)
+
+@pytest.mark.parametrize("M,N,K", [(1, 4096, 4096), (3, 6144, 4096), (16, 512, 512), (17, 1536, 512),
+                                   (32, 28672, 4096), (64, 4096, 14336), (65, 4096, 4096), (128, 256, 64),
+                                   (300, 6144, 4096), (513, 1024, 512), (2048, 4096, 4096), (129, 32000, 512),
+                                   (7, 128256, 4096)])
+def test_gemm_matches_fp32(M, N, K):
+    g = torch.Generator(device=DEV).manual_seed(M * 7 + N)
+    a = (torch.randn(M, K, generator=g, device=DEV)).bfloat16()
+    w = (torch.randn(N, K, generator=g, device=DEV) * 0.02).bfloat16()
+    ref = a.float() @ w.float().T
+    out = ops.gemm(a, w)
+    torch.cuda.synchronize()
+    assert rel_err(out, ref) < 5e-3
+
+
+@pytest.mark.parametrize("M", [4, 200])
+def test_gemm_residual_in_place(M):
+    N, K = 1024, 2048
+    g = torch.Generator(device=DEV).manual_seed(5)
+    a = torch.randn(M, K, generator=g, device=DEV).bfloat16()
+    w = (torch.randn(N, K, generator=g, device=DEV) * 0.02).bfloat16()
+    x = torch.randn(M, N, generator=g, device=DEV).bfloat16()
+    ref = a.float() @ w.float().T + x.float()
+    ops.gemm(a, w, out=x, residual=x)
+    torch.cuda.synchronize()
+    assert rel_err(x, ref) < 5e-3
+
+
+def test_gemm_split_k_workspace_stays_zeroed():
+    ws = torch.zeros(8 * 4096 + 1, dtype=torch.float32, device=DEV)
+    a = torch.randn(8, 4096, device=DEV).bfloat16()
+    w = (torch.randn(4096, 4096, device=DEV) * 0.02).bfloat16()
+    o1 = ops.gemm(a, w, workspace=ws)
+    o2 = ops.gemm(a, w, workspace=ws)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
+    assert torch.count_nonzero(ws) == 0
+
+
+# ---------------------------------------------------------------- K8 small ops
+
+def test_rmsnorm_silu_embedding_argmax():
+    g = torch.Generator(device=DEV).manual_seed(2)
+    x = torch.randn(33, 4096, generator=g, device=DEV).bfloat16()
+    r = torch.randn(33, 4096, generator=g, device=DEV).bfloat16()
+    w = (1 + 0.1 * torch.randn(4096, generator=g, device=DEV)).bfloat16()
+    y = torch.empty_like(x)
+    ro = torch.empty_like(x)
+    ops.rmsnorm(x, w, 1e-5, out=y, residual=r, resid_out=ro)
+    s = (x.float() + r.float()).bfloat16().float()
+    ref = s * torch.rsqrt(s.pow(2).mean(-1, keepdim=True) + 1e-5) * w.float()
+    assert rel_err(y, ref) < 4e-3
+    assert torch.equal(ro, (x.float() + r.float()).bfloat16())
+    gu = torch.randn(9, 2 * 1536, generator=g, device=DEV).bfloat16()
+    m = ops.silu_mul(gu)
+    ref = torch.nn.functional.silu(gu[:, :1536].float()) * gu[:, 1536:].float()
+    assert rel_err(m, ref) < 8e-3
+    table = torch.randn(1000, 512, generator=g, device=DEV).bfloat16()
+    ids = torch.tensor([3, 999, 0, 3], dtype=torch.int32, device=DEV)
+    assert torch.equal(ops.embedding(ids, table), table[ids.long()])
+    logits = torch.randn(5, 128256, generator=g, device=DEV).bfloat16()
+    logits[2, 77] = 100.0
+    logits[2, 99] = 100.0  # tie -> lowest index
+    am = ops.argmax(logits)
+    torch.cuda.synchronize()
+    assert am.tolist()[2] == 77
+    assert am.tolist() == [int(v) for v in logits.float().argmax(-1).tolist()[:2]] + [77] + \
+        [int(v) for v in logits.float().argmax(-1).tolist()[3:]]
+
+
+def test_decode_advance_drives_rows_and_records_history():
+    B = 3
+    dev = DEV
+    n_gen = torch.tensor([2, 4, 1], dtype=torch.int32, device=dev)
+    base = torch.tensor([10, 0, 31], dtype=torch.int32, device=dev)
+    first = torch.tensor([7, 8, 9], dtype=torch.int32, device=dev)
+    table = torch.tensor([[5, 6, -1], [1, -1, -1], [2, 3, -1]], dtype=torch.int32, device=dev)
+    step = torch.zeros(1, dtype=torch.int32, device=dev)
+    sampled = torch.zeros(B, dtype=torch.int32, device=dev)
+    tok, pos, slot, ctx = (torch.empty(B, dtype=torch.int32, device=dev) for _ in range(4))
+    hist = torch.zeros(B, 5, dtype=torch.int32, device=dev)
+    seen = []
+    for s in range(5):
+        ops.decode_advance(step, B, n_gen, base, first, sampled, table, 16, tok, pos, slot, ctx, hist, 5)
+        seen.append((tok.tolist(), pos.tolist(), slot.tolist(), ctx.tolist()))
+        sampled.copy_(tok + 100)
+    assert seen[0] == ([7, 8, 9], [10, 0, 31], [5 * 16 + 10, 16, 3 * 16 + 15], [11, 1, 32])
+    assert seen[1] == ([107, 108, 0], [11, 1, 0], [5 * 16 + 11, 17, -1], [12, 2, 0])
+    assert seen[4][2] == [-1, -1, -1]
+    h = hist.tolist()
+    assert h[0][:3] == [7, 107, 207] and h[2][:2] == [9, 109] and h[1][:5] == [8, 108, 208, 308, 408]

@@ -1,0 +1,122 @@
+"""Logits parity of the device Llama forward (tcgen05 GEMMs, paged
+attention, fused ops) against the fp32 CPU oracle, and KV-action
+invariance: preserve, swap round trip and discard-recompute leave the same
+KV behind (bit-identical for swap)."""
+
+import math
+
+import pytest
+import torch
+
+from conftest import cuda_available
+from oracle import llama_ref
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="needs a B200")]
+
+from paper_2512_14142_b200.gpu import ops  # noqa: E402
+from paper_2512_14142_b200.gpu.datapath import KvPool  # noqa: E402
+from paper_2512_14142_b200.gpu.model import PRESETS, LlamaRunner, LlamaWeights  # noqa: E402
+from paper_2512_14142_b200.host import (CacheLocation, RequestSpec, RequestState,  # noqa: E402
+                                        SegmentSpec, segment_token_ids)
+from paper_2512_14142_b200.host.engine import AdmittedMember  # noqa: E402
+
+DEV = "cuda"
+
+
+def rel(a, b):
+    a, b = a.float().cpu(), b.float().cpu()
+    return float((a - b).norm() / b.norm())
+
+
+def _prefill_one(runner, pool, ids, blocks, start=0):
+    T = len(ids)
+    pos = list(range(start, start + T))
+    slots = [blocks[p // 16] * 16 + p % 16 for p in pos]
+    d = lambda v: torch.tensor(v, dtype=torch.int32, device=DEV)  # noqa: E731
+    table = d([blocks]).view(1, -1)
+    return runner.prefill(d(ids), d(pos), d(slots), d([0, T]), table, d([start + T]),
+                          torch.tensor([T - 1], device=DEV), T, want_logits=True)
+
+
+@pytest.mark.parametrize("model", ["tiny", "small"])
+def test_prefill_then_decode_logits_match_oracle(model):
+    cfg = PRESETS[model]
+    w = LlamaWeights(cfg, seed=1)
+    pool = KvPool(cfg, 64)
+    runner = LlamaRunner(w, pool)
+    wc = w.to_cpu_dict()
+    ids = segment_token_ids("x", 1, 45, cfg.vocab)
+    blocks = [7, 3, 11, 20, 21]
+    tok, logits = _prefill_one(runner, pool, ids, blocks)
+    ref = llama_ref.forward(wc, cfg, ids)
+    assert rel(logits[0], ref[-1]) < 1e-2
+    assert int(tok[0]) == int(ref[-1].argmax())
+    # three decode steps through the paged cache
+    seq = list(ids)
+    nxt = int(tok[0])
+    d = lambda v: torch.tensor(v, dtype=torch.int32, device=DEV)  # noqa: E731
+    for step in range(3):
+        p = len(seq)
+        seq.append(nxt)
+        out, lg = runner.decode(d([nxt]), d([p]), d([blocks[p // 16] * 16 + p % 16]), d([blocks]).view(1, -1),
+                                d([p + 1]), want_logits=True)
+        ref = llama_ref.forward(wc, cfg, seq)[-1]
+        assert rel(lg[0], ref) < 1e-2, step
+        nxt = int(out[0])
+
+
+def test_chunked_prefill_equals_single_prefill():
+    cfg = PRESETS["small"]
+    w = LlamaWeights(cfg, seed=2)
+    pool = KvPool(cfg, 32)
+    runner = LlamaRunner(w, pool)
+    ids = segment_token_ids("y", 1, 70, cfg.vocab)
+    _, full = _prefill_one(runner, pool, ids, [1, 2, 3, 4, 5])
+    _prefill_one(runner, pool, ids[:50], [10, 11, 12, 13, 14])
+    _, tail = _prefill_one(runner, pool, ids[50:], [10, 11, 12, 13, 14], start=50)
+    assert rel(tail[0], full[0]) < 1e-2
+
+
+def test_kv_action_invariance_preserve_swap_discard():
+    """Segment 2 after segment 1 under the three KV actions."""
+    from gpu_util import datapath_for
+    spec = RequestSpec("inv", 0.0, (SegmentSpec(1, 40, 9, "Search", 1.0), SegmentSpec(2, 21, 6)))
+    results = {}
+    for action in ("preserve", "swap", "discard"):
+        dp = datapath_for(4000, model="small", seed=3)
+        st = RequestState(spec=spec)
+        dp.launch_batch([AdmittedMember(st, 1, CacheLocation.NONE, 0)])
+        st.kv_tokens = st.context_after(1)
+        st.cache_location = CacheLocation.GPU
+        st.current_segment = 2
+        rd = dp.reqs["inv"]
+        kv1 = torch.empty(st.kv_tokens * dp.pool.bytes_per_token, dtype=torch.uint8, pin_memory=True)
+        ops.swap_out(dp.pool.geo, dp.pool.data, rd.blocks, st.kv_tokens, kv1, stream=dp.compute)
+        prior = CacheLocation.GPU
+        if action == "swap":
+            st.swap_direction = "out"
+            dp.swap_out_begin(st)
+            dp.swap_out_done(st)
+            st.cache_location = CacheLocation.HOST
+            dp.swap_in_begin(st)
+            st.cache_location = CacheLocation.GPU
+            dp.swap_in_done(st)
+        elif action == "discard":
+            dp.drop(st)
+            st.kv_tokens = 0
+            st.cache_location = CacheLocation.DROPPED
+            prior = CacheLocation.DROPPED
+        dp.launch_batch([AdmittedMember(st, 2, prior, st.kv_tokens)])
+        dp.synchronize()
+        n = st.context_after(2)
+        kv2 = torch.empty(n * dp.pool.bytes_per_token, dtype=torch.uint8, pin_memory=True)
+        ops.swap_out(dp.pool.geo, dp.pool.data, dp.reqs["inv"].blocks, n, kv2, stream=dp.compute)
+        dp.synchronize()
+        toks = torch.cat([h.cpu() for h in dp.reqs["inv"].hist]).tolist()
+        results[action] = (kv1.clone(), kv2.clone(), toks)
+    p, s, d = results["preserve"], results["swap"], results["discard"]
+    assert torch.equal(p[1], s[1]) and p[2] == s[2]          # swap: bit-identical
+    kv_p = p[1].view(torch.bfloat16).float()
+    kv_d = d[1].view(torch.bfloat16).float()
+    assert float((kv_p - kv_d).norm() / kv_p.norm()) < 1e-2   # recompute: within tolerance
+    assert p[2][:49] == d[2][:49]                              # segment-1 context re-fed exactly
