@@ -183,8 +183,10 @@ ASTRAEA_API int astraea_paged_prefill_attention(const astraea_kv_geometry* g, co
  * C[M][N] = A[M][K] . W[N][K]^T (+ residual[M][N]), bf16 in, fp32 TMEM
  * accumulate, bf16 out. lda/ldw/ldc in elements. Prefill (M large) and decode
  * (M = batch) both run on tcgen05.mma; decode uses the swapped-operand form
- * (W rows on the MMA M axis) with split-K. workspace may be NULL when
- * astraea_gemm_workspace_bytes() returns 0. */
+ * (W rows on the MMA M axis) with deterministic split-K. workspace may be
+ * NULL when astraea_gemm_workspace_bytes() returns 0; otherwise it must be
+ * zero-filled once before first use (its arrival counters are reset by the
+ * kernel itself) and not shared by concurrently running GEMMs. */
 enum { ASTRAEA_EPI_NONE = 0, ASTRAEA_EPI_RESIDUAL = 1 };
 ASTRAEA_API size_t astraea_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K);
 ASTRAEA_API int astraea_gemm_bf16(const void* A_dev, int32_t lda, const void* W_dev, int32_t ldw,

@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(128) decode_kernel(const __grid_constant__ Dec
   constexpr int CPT = CPR / 8;              // chunks per score thread (8 threads per token)
   constexpr int TPH = 128 / G;              // PV threads per q head
   constexpr int DPT = D / TPH;              // dims per PV thread
-  static_assert(DPT >= 2 && DPT <= 8, "PV mapping");
+  static_assert(DPT >= 1 && DPT <= 8, "PV mapping");
 
   __shared__ __align__(128) bf16 ks[kStages][PAGE];
   __shared__ __align__(128) bf16 vs[kStages][PAGE];
@@ -149,9 +149,11 @@ __global__ void __launch_bounds__(128) decode_kernel(const __grid_constant__ Dec
         const float2 a0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
         const float2 a1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
         acc[0] += pr * a0.x; acc[1] += pr * a0.y; acc[2] += pr * a1.x; acc[3] += pr * a1.y;
-      } else {
+      } else if constexpr (DPT == 2) {
         const float2 a0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr));
         acc[0] += pr * a0.x; acc[1] += pr * a0.y;
+      } else {
+        acc[0] += pr * bf2f(*vr);
       }
     }
     m = mt;
@@ -166,9 +168,13 @@ __global__ void __launch_bounds__(128) decode_kernel(const __grid_constant__ Dec
 #pragma unroll
     for (int i = 0; i < DPT; ++i) o[i] = acc[i] * inv;
     bf16* dst = p.out + ((long long)b * p.Hq + hq) * D + pd;
+    if constexpr (DPT == 1) {
+      dst[0] = f2bf(o[0]);
+    } else {
 #pragma unroll
-    for (int i = 0; i < DPT; i += 2)
-      *reinterpret_cast<__nv_bfloat162*>(dst + i) = __floats2bfloat162_rn(o[i], o[i + 1]);
+      for (int i = 0; i < DPT; i += 2)
+        *reinterpret_cast<__nv_bfloat162*>(dst + i) = __floats2bfloat162_rn(o[i], o[i + 1]);
+    }
   } else {
     const long long row = ((long long)b * p.Hq + hq) * p.splits + split;
     const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -480,6 +486,8 @@ extern "C" int astraea_paged_decode_attention(const astraea_kv_geometry* g, cons
   else if (D == 64 && G == 4) LAUNCH_DEC(64, 4);
   else if (D == 64 && G == 8) LAUNCH_DEC(64, 8);
   else if (D == 128 && G == 2) LAUNCH_DEC(128, 2);
+  else if (D == 64 && G == 2) LAUNCH_DEC(64, 2);
+  else if (D == 128 && G == 1) LAUNCH_DEC(128, 1);
   else return ASTRAEA_EUNSUPPORTED;
 #undef LAUNCH_DEC
   ASTRAEA_CHECK_LAUNCH();

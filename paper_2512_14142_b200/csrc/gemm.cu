@@ -20,9 +20,9 @@
 //          rows of W; bf16 output (+ residual) stored directly.
 //   kCols  (decode, M <= 64): MMA M axis = rows of W (128 output features),
 //          N axis = the M tokens padded to 16/32/64 ("swap AB"), with
-//          split-K across CTAs so the weight stream covers all SMs; fp32
-//          partials are reduced with red.global.add into a zeroed workspace
-//          and a finalize kernel converts to bf16 (+ residual) and re-zeroes.
+//          split-K across CTAs so the weight stream covers all SMs; the
+//          last CTA of each tile reduces the fp32 partials in split order
+//          (deterministic) and applies the bf16 (+ residual) epilogue.
 #include <cuda.h>
 
 #include <mutex>
@@ -89,10 +89,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ void red_add_f32(float* p, float v) {
-  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
-}
-
 // UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups of
 // 1024 bytes (SBO), version 1 (sm_100).
 __device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
@@ -116,7 +112,8 @@ enum Orient { kRows = 0, kCols = 1 };
 struct GemmArgs {
   bf16* C;
   const bf16* residual;
-  float* ws;          // kCols: fp32 [M][N] partials
+  float* ws;          // kCols split-K: fp32 [splits][M][N] partials
+  int* counters;      // kCols split-K: per-tile arrival counters (zero between launches)
   int M, N, K, ldc;
   int kb_per_split;   // K blocks per CTA (split-K)
 };
@@ -235,18 +232,57 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     } else {
-      // kCols: TMEM lane = output feature, columns = tokens.
+      // kCols: TMEM lane = output feature, columns = tokens (M <= BN, one tile).
+      // Split-K partials are reduced deterministically: every split stores its
+      // fp32 partial; the last CTA of the tile to arrive sums them in split
+      // order and applies the epilogue (no atomics on data, no extra launch).
+      __shared__ int s_last;
       const int f = tile_a * kBM + row_in_tile;
+      const int splits = gridDim.z;
+      const bool fok = f < args.N;
+      if (splits == 1) {
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        float v[32];
-        tmem_ld32(lane_addr + c0, v);
-        if (f < args.N && nkb > 0) {
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
+          tmem_ld32(lane_addr + c0, v);
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
-            const int t = tile_b * BN + c0 + e;
-            if (t < args.M) red_add_f32(args.ws + (long long)t * args.N + f, v[e]);
+            const int t = c0 + e;
+            if (t < args.M && fok) {
+              float o = v[e];
+              if (args.residual) o += bf2f(args.residual[(long long)t * args.ldc + f]);
+              args.C[(long long)t * args.ldc + f] = f2bf(o);
+            }
           }
+        }
+      } else {
+        float* part = args.ws + (long long)split * args.M * args.N;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
+          tmem_ld32(lane_addr + c0, v);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const int t = c0 + e;
+            if (t < args.M && fok) __stcg(part + (long long)t * args.N + f, v[e]);
+          }
+        }
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (threadIdx.x == 64) s_last = atomicAdd(args.counters + tile_a, 1) == splits - 1;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (s_last) {
+          __threadfence();
+          if (fok) {
+            for (int t = 0; t < args.M; ++t) {
+              float o = 0.f;
+              for (int sp = 0; sp < splits; ++sp)
+                o += __ldcg(args.ws + ((long long)sp * args.M + t) * args.N + f);
+              if (args.residual) o += bf2f(args.residual[(long long)t * args.ldc + f]);
+              args.C[(long long)t * args.ldc + f] = f2bf(o);
+            }
+          }
+          if (threadIdx.x == 64) args.counters[tile_a] = 0;  // ready for the next launch
         }
       }
     }
@@ -254,19 +290,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
-}
-
-__global__ void splitk_finalize_kernel(float* __restrict__ ws, const bf16* __restrict__ residual,
-                                       bf16* __restrict__ C, int M, int N, int ldc) {
-  const long long total = (long long)M * N;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long m = i / N, n = i % N;
-    float v = ws[i];
-    ws[i] = 0.f;
-    if (residual) v += bf2f(residual[m * ldc + n]);
-    C[m * ldc + n] = f2bf(v);
-  }
 }
 
 // ---- host side ----------------------------------------------------------------------------
@@ -352,6 +375,8 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, dim3
   return 0;
 }
 
+constexpr int kColsMaxM = 64;
+
 // Decode path: split count that best fills the SMs (wave quantisation).
 int pick_splits(int tiles, int total_kb, int slots) {
   int best = 1;
@@ -369,13 +394,33 @@ int pick_splits(int tiles, int total_kb, int slots) {
   return best;
 }
 
-constexpr int kColsMaxM = 64;
+
+struct ColsPlan {
+  int bn, tiles, splits, kb_per_split;
+};
+
+ColsPlan cols_plan(int M, int N, int K) {
+  ColsPlan p;
+  p.bn = M <= 16 ? 16 : (M <= 32 ? 32 : 64);
+  p.tiles = (N + kBM - 1) / kBM;
+  const int total_kb = (K + kBK - 1) / kBK;
+  const int s = pick_splits(p.tiles, total_kb, 2 * num_sms());
+  p.kb_per_split = (total_kb + s - 1) / s;
+  p.splits = (total_kb + p.kb_per_split - 1) / p.kb_per_split;
+  return p;
+}
+
+size_t cols_ws_bytes(int M, int N, const ColsPlan& p) {
+  if (p.splits == 1) return 0;
+  const size_t counters = ((size_t)p.tiles * 4 + 255) / 256 * 256;
+  return counters + (size_t)p.splits * M * N * sizeof(float);
+}
 
 }  // namespace
 
 extern "C" size_t astraea_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K) {
-  (void)K;
-  return M <= kColsMaxM ? (size_t)M * N * sizeof(float) : 0;
+  if (M <= 0 || M > kColsMaxM || N <= 0 || K <= 0) return 0;
+  return cols_ws_bytes(M, N, cols_plan(M, N, K));
 }
 
 extern "C" int astraea_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, void* C, int32_t ldc,
@@ -387,11 +432,11 @@ extern "C" int astraea_gemm_bf16(const void* A, int32_t lda, const void* W, int3
   if (epilogue == ASTRAEA_EPI_NONE) residual = nullptr;
   if (M == 0) return ASTRAEA_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  const int total_kb = (K + kBK - 1) / kBK;
   GemmArgs a;
   a.C = (bf16*)C;
   a.residual = (const bf16*)residual;
-  a.ws = (float*)ws;
+  a.ws = nullptr;
+  a.counters = nullptr;
   a.M = M;
   a.N = N;
   a.K = K;
@@ -399,28 +444,23 @@ extern "C" int astraea_gemm_bf16(const void* A, int32_t lda, const void* W, int3
   CUtensorMap ma, mb;
   int rc;
   if (M <= kColsMaxM) {
-    // swap-AB: MMA A = W (128 features), MMA B = activations (BN tokens)
-    if (!ws || ws_bytes < (size_t)M * N * sizeof(float)) return ASTRAEA_EINVAL;
-    const int bn = M <= 16 ? 16 : (M <= 32 ? 32 : 64);
+    // swap-AB: MMA A = W (128 features), MMA B = activations (bn tokens)
+    const ColsPlan p = cols_plan(M, N, K);
+    const size_t need = cols_ws_bytes(M, N, p);
+    if (need) {
+      if (!ws || ws_bytes < need) return ASTRAEA_EINVAL;
+      a.counters = (int*)ws;
+      a.ws = (float*)((char*)ws + (((size_t)p.tiles * 4 + 255) / 256 * 256));
+    }
+    a.kb_per_split = p.kb_per_split;
     if ((rc = make_map(&ma, W, N, K, ldw, kBM))) return rc;
-    if ((rc = make_map(&mb, A, M, K, lda, bn))) return rc;
-    const int tiles = (N + kBM - 1) / kBM;
-    const int splits = pick_splits(tiles, total_kb, 2 * num_sms());
-    a.kb_per_split = (total_kb + splits - 1) / splits;
-    const int used_splits = (total_kb + a.kb_per_split - 1) / a.kb_per_split;
-    dim3 grid(tiles, 1, used_splits);
-    if (bn == 16) rc = launch<16, 8, kCols>(ma, mb, a, grid, st);
-    else if (bn == 32) rc = launch<32, 8, kCols>(ma, mb, a, grid, st);
-    else rc = launch<64, 6, kCols>(ma, mb, a, grid, st);
-    if (rc) return rc;
-    const long long total = (long long)M * N;
-    long long blocks = (total + 255) / 256;
-    if (blocks > 4LL * num_sms()) blocks = 4LL * num_sms();
-    splitk_finalize_kernel<<<(int)blocks, 256, 0, st>>>(a.ws, a.residual, a.C, M, N, ldc);
-    ASTRAEA_CHECK_LAUNCH();
-    return ASTRAEA_OK;
+    if ((rc = make_map(&mb, A, M, K, lda, p.bn))) return rc;
+    dim3 grid(p.tiles, 1, p.splits);
+    if (p.bn == 16) return launch<16, 8, kCols>(ma, mb, a, grid, st);
+    if (p.bn == 32) return launch<32, 8, kCols>(ma, mb, a, grid, st);
+    return launch<64, 6, kCols>(ma, mb, a, grid, st);
   }
-  a.kb_per_split = total_kb;
+  a.kb_per_split = (K + kBK - 1) / kBK;
   const int bn = (N % 256 == 0 && (long long)((M + kBM - 1) / kBM) * (N / 256) >= num_sms()) ? 256 : 128;
   if ((rc = make_map(&ma, A, M, K, lda, kBM))) return rc;
   if ((rc = make_map(&mb, W, N, K, ldw, bn))) return rc;

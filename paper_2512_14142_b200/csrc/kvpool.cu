@@ -194,6 +194,15 @@ static int swap_impl(bool out, const astraea_kv_geometry* g, const void* pool, v
     return ASTRAEA_OK;
   }
   if (mode != ASTRAEA_SWAP_KERNEL) return ASTRAEA_EINVAL;
+  {
+    // The SM path dereferences the slot over the host link: it must be pinned.
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, out ? slot_mut : slot) != cudaSuccess ||
+        (attr.type != cudaMemoryTypeHost && attr.type != cudaMemoryTypeManaged)) {
+      cudaGetLastError();
+      return ASTRAEA_EINVAL;
+    }
+  }
   char* slot_dev = (char*)mapped(out ? slot_mut : slot);
   const int grid = num_sms() * 2;
   for (int32_t first = 0; first < n_blocks; first += kSwapMaxIds) {

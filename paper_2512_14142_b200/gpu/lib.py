@@ -102,7 +102,13 @@ def check(status: int, what: str) -> None:
         raise DeviceError(f"{what} failed with status {status}: {msg}")
 
 
+_CUDA_OK = False
+
+
 def require_cuda():
+    global _CUDA_OK
+    if _CUDA_OK:
+        return _LIB
     import torch
 
     if not torch.cuda.is_available():
@@ -110,7 +116,9 @@ def require_cuda():
     major, minor = torch.cuda.get_device_capability()
     if major != 10:
         raise DeviceError(f"need an sm_100 (B200) device, found sm_{major}{minor}")
-    return load()
+    lib = load()
+    _CUDA_OK = True
+    return lib
 
 
 def ptr(t) -> int:

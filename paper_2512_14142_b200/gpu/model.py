@@ -25,6 +25,7 @@ from dataclasses import dataclass
 
 import torch
 
+from . import lib as L
 from . import ops
 
 
@@ -122,9 +123,14 @@ class LlamaRunner:
         dev = weights.embed.device
         cfg = self.cfg
         self.scale = 1.0 / math.sqrt(cfg.head_dim)
-        # split-K fp32 workspace for M <= 64 GEMMs (kept zeroed by the kernels)
-        self.gemm_ws = torch.zeros(64 * max(cfg.vocab, 2 * cfg.ffn, cfg.qkv_dim), dtype=torch.float32,
-                                   device=dev)
+        # split-K workspace for decode GEMMs (M <= 64): partials + arrival
+        # counters; zero-filled once, the kernel resets its counters.
+        d = cfg.hidden
+        shapes = [(cfg.qkv_dim, d), (d, cfg.num_q_heads * cfg.head_dim), (2 * cfg.ffn, d), (d, cfg.ffn),
+                  (cfg.vocab, d)]
+        lib = L.load()
+        need = max(lib.astraea_gemm_workspace_bytes(64, n, k) for n, k in shapes)
+        self.gemm_ws = torch.zeros(need // 4 + 64, dtype=torch.float32, device=dev)
         self.max_rows = max_rows
         self.dec_ws = None
         self.dec_ws_key = None

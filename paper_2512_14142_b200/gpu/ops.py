@@ -14,8 +14,24 @@ import torch
 from . import lib as L
 
 
+# Kernels launched through this module (the bench's ``gpu_launches`` claim).
+LAUNCHES = [0]
+
+
 def _s(stream):
     return L.stream_handle(stream)
+
+
+def _count(n=1):
+    LAUNCHES[0] += n
+
+
+def decode_splits(B, Hkv, max_blocks, sms=148):
+    """Mirror of the library's split choice (attention.cu decode_splits)."""
+    target = 4 * sms
+    want = max(1, min(-(-target // (B * Hkv)), max_blocks))
+    per = max(-(-max_blocks // want), 2)
+    return -(-max_blocks // per)
 
 
 def geometry(num_layers, num_kv_heads, head_dim, num_blocks, block_tokens=16) -> L.KvGeometry:
@@ -41,6 +57,7 @@ def gemm(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None,
         L.ptr(residual), L.EPI_RESIDUAL if residual is not None else L.EPI_NONE,
         L.ptr(workspace), 0 if workspace is None else workspace.numel() * workspace.element_size(),
         _s(stream)), "gemm_bf16")
+    _count()
     return out
 
 
@@ -51,6 +68,7 @@ def rmsnorm(x, weight, eps, out=None, residual=None, resid_out=None, stream=None
         out = torch.empty_like(x)
     L.check(lib.astraea_rmsnorm(L.ptr(x), L.ptr(residual), L.ptr(weight), L.ptr(out), L.ptr(resid_out),
                                 rows, dim, eps, _s(stream)), "rmsnorm")
+    _count()
     return out
 
 
@@ -61,6 +79,7 @@ def silu_mul(gu, out=None, stream=None):
     if out is None:
         out = torch.empty(T, F, dtype=gu.dtype, device=gu.device)
     L.check(lib.astraea_silu_mul(L.ptr(gu), L.ptr(out), T, F, _s(stream)), "silu_mul")
+    _count()
     return out
 
 
@@ -71,6 +90,7 @@ def embedding(ids, table, out=None, stream=None):
     if out is None:
         out = torch.empty(T, dim, dtype=table.dtype, device=table.device)
     L.check(lib.astraea_embedding(L.ptr(ids), L.ptr(table), L.ptr(out), T, dim, _s(stream)), "embedding")
+    _count()
     return out
 
 
@@ -80,6 +100,7 @@ def argmax(logits, out=None, stream=None):
     if out is None:
         out = torch.empty(rows, dtype=torch.int32, device=logits.device)
     L.check(lib.astraea_argmax(L.ptr(logits), rows, vocab, L.ptr(out), _s(stream)), "argmax")
+    _count()
     return out
 
 
@@ -88,6 +109,7 @@ def rope_kv_append(geo, pool, layer, qkv, num_q_heads, positions, slots, theta, 
     L.check(lib.astraea_rope_kv_append(ctypes.byref(geo), L.ptr(pool), layer, L.ptr(qkv), qkv.shape[0],
                                        num_q_heads, L.ptr(positions), L.ptr(slots), theta, _s(stream)),
             "rope_kv_append")
+    _count()
 
 
 def decode_attention(geo, pool, layer, q, q_row_stride, B, num_q_heads, table, ctx, scale, out,
@@ -97,6 +119,7 @@ def decode_attention(geo, pool, layer, q, q_row_stride, B, num_q_heads, table, c
         ctypes.byref(geo), L.ptr(pool), layer, L.ptr(q), q_row_stride, B, num_q_heads, L.ptr(table),
         table.shape[1], L.ptr(ctx), scale, L.ptr(out), L.ptr(workspace),
         workspace.numel() * workspace.element_size(), _s(stream)), "paged_decode_attention")
+    _count(1 + (decode_splits(B, geo.num_kv_heads, table.shape[1]) > 1))
     return out
 
 
@@ -113,6 +136,7 @@ def prefill_attention(geo, pool, layer, q, q_row_stride, cu_q, S, max_q_len, num
         ctypes.byref(geo), L.ptr(pool), layer, L.ptr(q), q_row_stride, L.ptr(cu_q), S, max_q_len,
         num_q_heads, L.ptr(table), table.shape[1], L.ptr(ctx), scale, L.ptr(out), _s(stream)),
         "paged_prefill_attention")
+    _count()
     return out
 
 
@@ -121,6 +145,7 @@ def block_table_build(csr_ptr, csr_ids, rows, ctx_src, max_blocks, table, ctx, s
     L.check(lib.astraea_block_table_build(L.ptr(csr_ptr), L.ptr(csr_ids), L.ptr(rows), L.ptr(ctx_src),
                                           rows.shape[0], max_blocks, L.ptr(table), L.ptr(ctx), _s(stream)),
             "block_table_build")
+    _count()
 
 
 def decode_advance(step, B, n_gen, base_pos, first_tok, sampled, table, block_tokens, tokens, positions,
@@ -130,6 +155,7 @@ def decode_advance(step, B, n_gen, base_pos, first_tok, sampled, table, block_to
         L.ptr(step), B, L.ptr(n_gen), L.ptr(base_pos), L.ptr(first_tok), L.ptr(sampled), L.ptr(table),
         table.shape[1], block_tokens, L.ptr(tokens), L.ptr(positions), L.ptr(slots), L.ptr(ctx),
         L.ptr(hist), hist_stride, _s(stream)), "decode_advance")
+    _count()
 
 
 def swap_out(geo, pool, block_ids, n_tokens, slot, mode=L.SWAP_KERNEL, stream=None):
@@ -137,6 +163,7 @@ def swap_out(geo, pool, block_ids, n_tokens, slot, mode=L.SWAP_KERNEL, stream=No
     ids = L.i32_array(block_ids)
     L.check(lib.astraea_kv_swap_out(ctypes.byref(geo), L.ptr(pool), ids, len(block_ids), n_tokens,
                                     L.ptr(slot), mode, _s(stream)), "kv_swap_out")
+    _count(-(-len(block_ids) // 900) if mode == L.SWAP_KERNEL else 0)
 
 
 def swap_in(geo, pool, block_ids, n_tokens, slot, mode=L.SWAP_KERNEL, stream=None):
@@ -144,6 +171,7 @@ def swap_in(geo, pool, block_ids, n_tokens, slot, mode=L.SWAP_KERNEL, stream=Non
     ids = L.i32_array(block_ids)
     L.check(lib.astraea_kv_swap_in(ctypes.byref(geo), L.ptr(pool), ids, len(block_ids), n_tokens,
                                    L.ptr(slot), mode, _s(stream)), "kv_swap_in")
+    _count(-(-len(block_ids) // 900) if mode == L.SWAP_KERNEL else 0)
 
 
 def copy_blocks(geo, pool, src_ids, dst_ids, stream=None):

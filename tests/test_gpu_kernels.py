@@ -37,7 +37,7 @@ def make_pool(nb, Lyr, Hkv, D, seed=0):
 @pytest.mark.parametrize("Lyr,Hkv,D,n_tokens", [(4, 2, 64, 1), (4, 2, 64, 17), (4, 2, 64, 300),
                                                 (32, 8, 128, 1000), (80, 1, 128, 129)])
 def test_swap_out_matches_oracle_and_round_trips_bit_exact(mode, Lyr, Hkv, D, n_tokens):
-    nb_total = 96
+    nb_total = 160
     pool, geo = make_pool(nb_total, Lyr, Hkv, D, seed=n_tokens)
     nb = (n_tokens + 15) // 16
     rng = np.random.default_rng(n_tokens)
@@ -54,7 +54,7 @@ def test_swap_out_matches_oracle_and_round_trips_bit_exact(mode, Lyr, Hkv, D, n_
     dst = [b for b in rng.permutation(nb_total).tolist() if b not in src][:nb]
     before = pool.clone()
     ops.swap_in(geo, pool, dst, n_tokens, slot, mode)
-    slot2 = torch.zeros_like(slot)
+    slot2 = torch.zeros(slot.shape, dtype=torch.uint8, pin_memory=True)
     ops.swap_out(geo, pool, dst, n_tokens, slot2, mode)
     torch.cuda.synchronize()
     assert torch.equal(slot, slot2)
@@ -72,6 +72,8 @@ def test_swap_rejects_bad_arguments():
         ops.swap_out(geo, pool, [0, 1], 100, slot)          # 100 tokens need 7 blocks
     with pytest.raises(DeviceError):
         ops.swap_out(geo, pool, [0, 99], 20, slot)          # block id out of range
+    with pytest.raises(DeviceError):
+        ops.swap_out(geo, pool, [0, 1], 20, torch.zeros(slot.shape, dtype=torch.uint8))  # pageable slot
 
 
 def test_copy_blocks():
@@ -224,15 +226,17 @@ def test_gemm_residual_in_place(M):
     assert rel_err(x, ref) < 5e-3
 
 
-def test_gemm_split_k_workspace_stays_zeroed():
-    ws = torch.zeros(8 * 4096 + 1, dtype=torch.float32, device=DEV)
+def test_gemm_split_k_is_deterministic_and_resets_counters():
+    from paper_2512_14142_b200.gpu import lib as L
+    need = L.load().astraea_gemm_workspace_bytes(8, 4096, 4096)
+    assert need > 0  # this shape uses split-K
+    ws = torch.zeros(need // 4 + 1, dtype=torch.float32, device=DEV)
     a = torch.randn(8, 4096, device=DEV).bfloat16()
     w = (torch.randn(4096, 4096, device=DEV) * 0.02).bfloat16()
-    o1 = ops.gemm(a, w, workspace=ws)
-    o2 = ops.gemm(a, w, workspace=ws)
+    outs = [ops.gemm(a, w, workspace=ws) for _ in range(5)]
     torch.cuda.synchronize()
-    assert torch.equal(o1, o2)
-    assert torch.count_nonzero(ws) == 0
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
+    assert torch.count_nonzero(ws[:32]) == 0   # arrival counters (4096/128 = 32 tiles) back to zero
 
 
 # ---------------------------------------------------------------- K8 small ops
