@@ -410,10 +410,14 @@ ColsPlan cols_plan(int M, int N, int K) {
   return p;
 }
 
+// Workspace layout for split-K: a fixed counter region shared by every GEMM
+// shape (so GEMMs of different tile counts can reuse one workspace in
+// stream order without clobbering each other's counters), then partials.
+constexpr size_t kCounterBytes = 16384 * sizeof(int);
+
 size_t cols_ws_bytes(int M, int N, const ColsPlan& p) {
   if (p.splits == 1) return 0;
-  const size_t counters = ((size_t)p.tiles * 4 + 255) / 256 * 256;
-  return counters + (size_t)p.splits * M * N * sizeof(float);
+  return kCounterBytes + (size_t)p.splits * M * N * sizeof(float);
 }
 
 }  // namespace
@@ -449,8 +453,9 @@ extern "C" int astraea_gemm_bf16(const void* A, int32_t lda, const void* W, int3
     const size_t need = cols_ws_bytes(M, N, p);
     if (need) {
       if (!ws || ws_bytes < need) return ASTRAEA_EINVAL;
+      if ((size_t)p.tiles * sizeof(int) > kCounterBytes) return ASTRAEA_EUNSUPPORTED;
       a.counters = (int*)ws;
-      a.ws = (float*)((char*)ws + (((size_t)p.tiles * 4 + 255) / 256 * 256));
+      a.ws = (float*)((char*)ws + kCounterBytes);
     }
     a.kb_per_split = p.kb_per_split;
     if ((rc = make_map(&ma, W, N, K, ldw, kBM))) return rc;

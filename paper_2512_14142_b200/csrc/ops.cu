@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(1024) argmax_kernel(const bf16* __restrict__ l
         bidx = oi;
       }
     }
-    if (threadIdx.x == 0) out[row] = bidx;
+    if (threadIdx.x == 0) out[row] = bidx < vocab ? bidx : 0;  // all-NaN row: never emit an invalid id
   }
 }
 

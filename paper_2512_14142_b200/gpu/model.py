@@ -137,11 +137,10 @@ class LlamaRunner:
         self.device = dev
 
     def _dec_ws(self, B, max_blocks):
-        key = (B, max_blocks)
-        if self.dec_ws_key is None or B * max_blocks > self.dec_ws_key[0] * self.dec_ws_key[1]:
+        need = L.load().astraea_decode_workspace_bytes(B, self.cfg.num_q_heads, self.cfg.head_dim, max_blocks)
+        if self.dec_ws is None or self.dec_ws.numel() * 4 < need:
             self.dec_ws = ops.decode_workspace(B, self.cfg.num_q_heads, self.cfg.head_dim, max_blocks,
                                                self.device)
-            self.dec_ws_key = key
         return self.dec_ws
 
     def _layers(self, x, positions, slots, attend, stream=None):

@@ -239,6 +239,22 @@ def test_gemm_split_k_is_deterministic_and_resets_counters():
     assert torch.count_nonzero(ws[:32]) == 0   # arrival counters (4096/128 = 32 tiles) back to zero
 
 
+def test_split_k_gemms_of_different_shapes_share_one_workspace():
+    """Regression: partials of one shape must not clobber another's counters."""
+    from paper_2512_14142_b200.gpu import lib as L
+    lib = L.load()
+    shapes = [(6144, 4096), (128256, 4096), (4096, 4096), (4096, 14336)]
+    need = max(lib.astraea_gemm_workspace_bytes(4, n, k) for n, k in shapes)
+    ws = torch.zeros(need // 4 + 1, dtype=torch.float32, device=DEV)
+    g = torch.Generator(device=DEV).manual_seed(9)
+    for rep in range(2):
+        for n, k in shapes:
+            a = torch.randn(4, k, generator=g, device=DEV).bfloat16()
+            w = (torch.randn(n, k, generator=g, device=DEV) * 0.02).bfloat16()
+            out = ops.gemm(a, w, workspace=ws)
+            assert rel_err(out, a.float() @ w.float().T) < 5e-3, (rep, n, k)
+
+
 # ---------------------------------------------------------------- K8 small ops
 
 def test_rmsnorm_silu_embedding_argmax():
