@@ -154,7 +154,9 @@ ASTRAEA_API int astraea_rope_kv_append(const astraea_kv_geometry* g, void* pool_
  * holds [Hq][D] (so q can be read in place from the fused QKV rows);
  * table_dev[B][max_blocks];
  * ctx_dev[B] = tokens visible to the row (0 -> output zeros). out_dev[B][Hq][D].
- * workspace: float buffer, astraea_decode_workspace_bytes(...) bytes. */
+ * workspace: astraea_decode_workspace_bytes(...) bytes, zero-filled once
+ * before first use (it holds split arrival counters the kernel resets);
+ * splits of long contexts are merged inside the same launch. */
 ASTRAEA_API size_t astraea_decode_workspace_bytes(int32_t B, int32_t num_q_heads, int32_t head_dim,
                                       int32_t max_blocks);
 ASTRAEA_API int astraea_paged_decode_attention(const astraea_kv_geometry* g, const void* pool_dev,

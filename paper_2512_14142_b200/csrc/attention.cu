@@ -7,8 +7,8 @@
 //   (block_tokens x head_dim bf16, contiguous in the pool) are staged into a
 //   shared-memory ring with cp.async.bulk + mbarrier (TMA bulk engine); the
 //   GQA group's q heads share every staged page. Scores are reduced with
-//   warp shuffles, softmax is online in the exp2 domain, and splits are
-//   merged by a log-sum-exp combine kernel.
+//   warp shuffles, softmax is online in the exp2 domain, and context splits
+//   are merged (log-sum-exp, split order) by the last split CTA to finish.
 //
 // K7 prefill: the recompute-on-resume prefill (simulator.py:335-336),
 //   flash-attention style on mma.sync m16n8k16 tensor-core tiles: one CTA
@@ -36,6 +36,7 @@ struct DecodeParams {
   long long q_stride;
   float* ws_o;     // [B][Hq][splits][D]
   float* ws_lse;   // [B][Hq][splits]
+  int* counters;   // [B][Hkv] split arrival counters (zero between launches)
   long long block_el;  // elements per pool block
   int layer, Hkv, Hq, max_blocks, blocks_per_split, splits;
   float scale_log2;
@@ -58,6 +59,8 @@ __global__ void __launch_bounds__(128) decode_kernel(const __grid_constant__ Dec
 
   const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int tid = threadIdx.x;
+  pdl_wait();
+  pdl_launch();
   const int ctx = p.ctx[b];
   const int nblk = (ctx + kBT - 1) / kBT;
   const int b0 = split * p.blocks_per_split;
@@ -176,33 +179,44 @@ __global__ void __launch_bounds__(128) decode_kernel(const __grid_constant__ Dec
         *reinterpret_cast<__nv_bfloat162*>(dst + i) = __floats2bfloat162_rn(o[i], o[i + 1]);
     }
   } else {
+    // Split-K over the context: store this split's normalised partial and
+    // log-sum-exp; the last split CTA of (row, kv head) to arrive merges all
+    // splits in split order (deterministic) and writes the G output heads.
+    __shared__ int s_last;
     const long long row = ((long long)b * p.Hq + hq) * p.splits + split;
     const float inv = l > 0.f ? 1.f / l : 0.f;
     float* dst = p.ws_o + row * D + pd;
 #pragma unroll
-    for (int i = 0; i < DPT; ++i) dst[i] = acc[i] * inv;
-    if ((tid % TPH) == 0) p.ws_lse[row] = l > 0.f ? m + log2f(l) : -INFINITY;
-  }
-}
-
-template <int D>
-__global__ void decode_combine_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
-                                      int splits, bf16* __restrict__ out) {
-  const long long bh = blockIdx.x;
-  const float* lse = ws_lse + bh * splits;
-  float mx = -INFINITY;
-  for (int s = 0; s < splits; ++s) mx = fmaxf(mx, lse[s]);
-  for (int d = threadIdx.x; d < D; d += blockDim.x) {
-    float num = 0.f, den = 0.f;
-    if (mx != -INFINITY) {
-      for (int s = 0; s < splits; ++s) {
-        if (lse[s] == -INFINITY) continue;
-        const float w = exp2f(lse[s] - mx);
-        num += w * ws_o[(bh * splits + s) * D + d];
-        den += w;
+    for (int i = 0; i < DPT; ++i) __stcg(dst + i, acc[i] * inv);
+    if ((tid % TPH) == 0) __stcg(p.ws_lse + row, l > 0.f ? m + log2f(l) : -INFINITY);
+    __threadfence();
+    __syncthreads();
+    int* ctr = p.counters + (long long)b * p.Hkv + h;
+    if (tid == 0) s_last = atomicAdd(ctr, 1) == p.splits - 1;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      const long long row0 = ((long long)b * p.Hq + hq) * p.splits;
+      float mx = -INFINITY;
+      for (int sp = 0; sp < p.splits; ++sp) mx = fmaxf(mx, __ldcg(p.ws_lse + row0 + sp));
+      float num[DPT], den = 0.f;
+#pragma unroll
+      for (int i = 0; i < DPT; ++i) num[i] = 0.f;
+      if (mx != -INFINITY) {
+        for (int sp = 0; sp < p.splits; ++sp) {
+          const float ls = __ldcg(p.ws_lse + row0 + sp);
+          if (ls == -INFINITY) continue;
+          const float w = exp2f(ls - mx);
+          den += w;
+#pragma unroll
+          for (int i = 0; i < DPT; ++i) num[i] += w * __ldcg(p.ws_o + (row0 + sp) * D + pd + i);
+        }
       }
+      bf16* out = p.out + ((long long)b * p.Hq + hq) * D + pd;
+#pragma unroll
+      for (int i = 0; i < DPT; ++i) out[i] = f2bf(den > 0.f ? num[i] / den : 0.f);
+      if (tid == 0) *ctr = 0;
     }
-    out[bh * D + d] = f2bf(den > 0.f ? num / den : 0.f);
   }
 }
 
@@ -269,6 +283,8 @@ __global__ void __launch_bounds__(128) prefill_kernel(const __grid_constant__ Pr
   bf16* vs = ks + 2 * kKT * D;                            // [2][64][D]
 
   const int s = blockIdx.z, hq = blockIdx.y, qt = blockIdx.x;
+  pdl_wait();
+  pdl_launch();
   const int q_begin = p.cu_q[s], len = p.cu_q[s + 1] - q_begin;
   if (qt * kQT >= len) return;
   const int ctx = p.ctx[s];
@@ -440,10 +456,13 @@ int decode_splits(int B, int Hkv, int max_blocks, int* bps) {
 
 }  // namespace
 
+// Decode workspace: [counters: 4096 ints][partials o: B*Hq*splits*D][lse: B*Hq*splits].
+constexpr size_t kDecCounterBytes = 4096 * sizeof(int);
+
 extern "C" size_t astraea_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t D, int32_t max_blocks) {
   // Upper bound over any Hkv: splits <= max_blocks / 2 + 1.
   const size_t splits = (size_t)max_blocks / 2 + 1;
-  return (size_t)B * Hq * splits * (D + 1) * sizeof(float);
+  return kDecCounterBytes + (size_t)B * Hq * splits * (D + 1) * sizeof(float);
 }
 
 extern "C" int astraea_paged_decode_attention(const astraea_kv_geometry* g, const void* pool,
@@ -474,13 +493,15 @@ extern "C" int astraea_paged_decode_attention(const astraea_kv_geometry* g, cons
   int bps = 0;
   p.splits = decode_splits(B, Hkv, max_blocks, &bps);
   p.blocks_per_split = bps;
-  const size_t need = (size_t)B * Hq * p.splits * (D + 1) * sizeof(float);
-  if (p.splits > 1 && (!ws || ws_bytes < need)) return ASTRAEA_EINVAL;
-  p.ws_o = (float*)ws;
+  const size_t need = kDecCounterBytes + (size_t)B * Hq * p.splits * (D + 1) * sizeof(float);
+  if (p.splits > 1 && (!ws || ws_bytes < need || (size_t)B * Hkv * sizeof(int) > kDecCounterBytes))
+    return ASTRAEA_EINVAL;
+  p.counters = (int*)ws;
+  p.ws_o = (float*)((char*)ws + kDecCounterBytes);
   p.ws_lse = p.ws_o + (size_t)B * Hq * p.splits * D;
   dim3 grid(p.splits, Hkv, B);
   cudaStream_t st = (cudaStream_t)stream;
-#define LAUNCH_DEC(DD, GG) decode_kernel<DD, GG><<<grid, 128, 0, st>>>(p)
+#define LAUNCH_DEC(DD, GG) ASTRAEA_TRY(launch_k(decode_kernel<DD, GG>, grid, dim3(128), 0, st, p))
   if (D == 128 && G == 4) LAUNCH_DEC(128, 4);
   else if (D == 128 && G == 8) LAUNCH_DEC(128, 8);
   else if (D == 64 && G == 4) LAUNCH_DEC(64, 4);
@@ -491,13 +512,6 @@ extern "C" int astraea_paged_decode_attention(const astraea_kv_geometry* g, cons
   else return ASTRAEA_EUNSUPPORTED;
 #undef LAUNCH_DEC
   ASTRAEA_CHECK_LAUNCH();
-  if (p.splits > 1) {
-    if (D == 128)
-      decode_combine_kernel<128><<<B * Hq, 128, 0, st>>>(p.ws_o, p.ws_lse, p.splits, p.out);
-    else
-      decode_combine_kernel<64><<<B * Hq, 64, 0, st>>>(p.ws_o, p.ws_lse, p.splits, p.out);
-    ASTRAEA_CHECK_LAUNCH();
-  }
   return ASTRAEA_OK;
 }
 
@@ -536,9 +550,9 @@ extern "C" int astraea_paged_prefill_attention(const astraea_kv_geometry* g, con
       ASTRAEA_TRY(cudaFuncSetAttribute(prefill_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr = true;
     }
-    prefill_kernel<128><<<grid, 128, smem, st>>>(p);
+    ASTRAEA_TRY(launch_k(prefill_kernel<128>, grid, dim3(128), smem, st, p));
   } else if (D == 64) {
-    prefill_kernel<64><<<grid, 128, smem, st>>>(p);
+    ASTRAEA_TRY(launch_k(prefill_kernel<64>, grid, dim3(128), smem, st, p));
   } else {
     return ASTRAEA_EUNSUPPORTED;
   }

@@ -25,6 +25,7 @@
 //          (deterministic) and applies the bf16 (+ residual) epilogue.
 #include <cuda.h>
 
+#include <algorithm>
 #include <mutex>
 #include <unordered_map>
 
@@ -161,11 +162,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  pdl_launch();
   if (warp == 0) {
     if (lane == 0) {
-      for (int i = 0; i < nkb; ++i) {
+      // Weights (map_b) do not depend on the previous kernel: prefetch the
+      // first stages before the grid-dependency wait.
+      const int pre = min(nkb, STAGES);
+      for (int i = 0; i < pre; ++i) {
+        mbar_arrive_expect_tx(&full[i], A_BYTES + B_BYTES);
+        tma_load_2d(sb + i * B_BYTES, &map_b, &full[i], (kb0 + i) * kBK, tile_b * BN);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i) tma_load_2d(sa + i * A_BYTES, &map_a, &full[i], (kb0 + i) * kBK, tile_a * kBM);
+      for (int i = pre; i < nkb; ++i) {
         const int s = i % STAGES;
-        if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
+        mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
         mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
         const int kc = (kb0 + i) * kBK;
         tma_load_2d(sa + s * A_BYTES, &map_a, &full[s], kc, tile_a * kBM);
@@ -173,6 +184,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
+    pdl_wait();
     constexpr uint32_t idesc = instr_desc(BN);
     for (int i = 0; i < nkb; ++i) {
       const int s = i % STAGES;
@@ -194,6 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (nkb == 0 && lane == 0) mbar_arrive(done);
   } else {
     // epilogue: warps 2..5 -> TMEM lane quarter (warp % 4)
+    pdl_wait();
     const int quarter = warp & 3;
     mbar_wait(done, 0);
     tc_fence_after();
@@ -231,59 +244,195 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-    } else {
-      // kCols: TMEM lane = output feature, columns = tokens (M <= BN, one tile).
-      // Split-K partials are reduced deterministically: every split stores its
-      // fp32 partial; the last CTA of the tile to arrive sums them in split
-      // order and applies the epilogue (no atomics on data, no extra launch).
-      __shared__ int s_last;
-      const int f = tile_a * kBM + row_in_tile;
-      const int splits = gridDim.z;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
+}
+
+// ---------------------------------------------------------------------------
+// Decode GEMM: persistent stream-K on tcgen05 (swap-AB orientation).
+//
+// MMA A = W rows (128 output features per tile), MMA B = the M <= 64 tokens
+// (BN = 16/32/64). The tiles x k-blocks work units are split evenly over one
+// CTA per SM, so every SM streams the same number of weight bytes (the
+// roofline of a decode step is the weight stream). A CTA walks its units
+// in order: the TMA ring runs continuously across tile boundaries, the MMA
+// warp accumulates each tile *segment* into one of two TMEM accumulators,
+// and the epilogue drains the other. Segments that cover a whole tile are
+// written directly; split tiles are fixed up deterministically -- each
+// segment stores an fp32 partial, the last to arrive sums them in segment
+// order and applies the bf16 (+ residual) epilogue.
+// ---------------------------------------------------------------------------
+struct SkArgs {
+  bf16* C;
+  const bf16* residual;
+  float* ws;        // [tiles][maxseg][M][128] partials
+  int* counters;    // [tiles] arrival counters, zero between launches
+  int M, N, K, ldc;
+  int tiles, kbs, grid, maxseg;
+  long long units;
+};
+
+__device__ __forceinline__ int sk_owner(long long u, long long units, int grid) {
+  return (int)(((u + 1) * grid - 1) / units);
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 2)
+    gemm_streamk_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
+                        const __grid_constant__ SkArgs args) {
+  constexpr int A_BYTES = kBM * kBK * 2;
+  constexpr int B_BYTES = BN * kBK * 2;
+  constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ int s_last;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cta = blockIdx.x;
+  const long long U = args.units;
+  const long long u0 = (long long)cta * U / args.grid;
+  const long long u1 = (long long)(cta + 1) * U / args.grid;
+  const int KB = args.kbs;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  pdl_launch();
+  if (warp == 0) {
+    if (lane == 0) {
+      // Weight tiles are independent of the previous kernel: stream the first
+      // STAGES of them while the predecessor drains, then wait for it and
+      // fetch the matching activation tiles.
+      const int pre = (int)(u1 - u0 < STAGES ? u1 - u0 : STAGES);
+      for (int i = 0; i < pre; ++i) {
+        const long long u = u0 + i;
+        mbar_arrive_expect_tx(&full[i], A_BYTES + B_BYTES);
+        tma_load_2d(sa + i * A_BYTES, &map_w, &full[i], (int)(u % KB) * kBK, (int)(u / KB) * kBM);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i) tma_load_2d(sb + i * B_BYTES, &map_x, &full[i], (int)((u0 + i) % KB) * kBK, 0);
+      int i = pre;
+      for (long long u = u0 + pre; u < u1; ++u, ++i) {
+        const int s = i % STAGES;
+        mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
+        mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
+        const int tile = (int)(u / KB), kc = (int)(u % KB) * kBK;
+        tma_load_2d(sa + s * A_BYTES, &map_w, &full[s], kc, tile * kBM);
+        tma_load_2d(sb + s * B_BYTES, &map_x, &full[s], kc, 0);
+      }
+    }
+  } else if (warp == 1) {
+    pdl_wait();
+    constexpr uint32_t idesc = instr_desc(BN);
+    int i = 0, seg = 0;
+    for (long long u = u0; u < u1; ++seg) {
+      const long long tile = u / KB;
+      const long long seg_end = min(u1, (tile + 1) * KB);
+      const int buf = seg & 1;
+      if (seg >= 2) mbar_wait(&tempty[buf], ((seg >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t acc = tmem + buf * BN;
+      const long long seg_begin = u;
+      for (; u < seg_end; ++u, ++i) {
+        const int s = i % STAGES;
+        mbar_wait(&full[s], (i / STAGES) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint64_t da = smem_desc_sw128(sa + s * A_BYTES);
+          const uint64_t db = smem_desc_sw128(sb + s * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            mma_bf16(acc, da + 2 * k, db + 2 * k, idesc, (u != seg_begin || k != 0) ? 1u : 0u);
+          mma_commit(&empty[s]);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) mma_commit(&tfull[buf]);
+      __syncwarp();
+    }
+  } else {
+    pdl_wait();
+    const int quarter = warp & 3;
+    const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
+    const int row = quarter * 32 + lane;  // feature within the tile
+    int seg = 0;
+    for (long long u = u0; u < u1; ++seg) {
+      const long long tile = u / KB;
+      const long long seg_end = min(u1, (tile + 1) * KB);
+      const bool whole = (u == tile * KB) && (seg_end == (tile + 1) * KB);
+      u = seg_end;
+      const int buf = seg & 1;
+      mbar_wait(&tfull[buf], (seg >> 1) & 1);
+      tc_fence_after();
+      float v[BN < 32 ? 32 : BN];
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 32) tmem_ld32(lane_addr + buf * BN + c0, v + c0);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+      const int f = (int)tile * kBM + row;
       const bool fok = f < args.N;
-      if (splits == 1) {
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-          float v[32];
-          tmem_ld32(lane_addr + c0, v);
+      if (whole) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const int t = c0 + e;
-            if (t < args.M && fok) {
-              float o = v[e];
-              if (args.residual) o += bf2f(args.residual[(long long)t * args.ldc + f]);
-              args.C[(long long)t * args.ldc + f] = f2bf(o);
-            }
+        for (int t = 0; t < BN; ++t) {
+          if (t < args.M && fok) {
+            float o = v[t];
+            if (args.residual) o += bf2f(args.residual[(long long)t * args.ldc + f]);
+            args.C[(long long)t * args.ldc + f] = f2bf(o);
           }
         }
-      } else {
-        float* part = args.ws + (long long)split * args.M * args.N;
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-          float v[32];
-          tmem_ld32(lane_addr + c0, v);
+        continue;
+      }
+      const long long first_u = tile * KB;
+      const int c_first = sk_owner(first_u, U, args.grid);
+      const int nseg = sk_owner(first_u + KB - 1, U, args.grid) - c_first + 1;
+      const int sidx = cta - c_first;
+      float* part = args.ws + ((tile * args.maxseg + sidx) * (long long)args.M) * kBM;
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const int t = c0 + e;
-            if (t < args.M && fok) __stcg(part + (long long)t * args.N + f, v[e]);
-          }
-        }
+      for (int t = 0; t < BN; ++t)
+        if (t < args.M) __stcg(part + (long long)t * kBM + row, v[t]);
+      __threadfence();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (threadIdx.x == 64) s_last = atomicAdd(args.counters + tile, 1) == nseg - 1;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (s_last) {
         __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (threadIdx.x == 64) s_last = atomicAdd(args.counters + tile_a, 1) == splits - 1;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (s_last) {
-          __threadfence();
+        const float* base = args.ws + (tile * args.maxseg * (long long)args.M) * kBM + row;
+        for (int t = 0; t < args.M; ++t) {
+          float o = 0.f;
+          for (int sg = 0; sg < nseg; ++sg) o += __ldcg(base + ((long long)sg * args.M + t) * kBM);
           if (fok) {
-            for (int t = 0; t < args.M; ++t) {
-              float o = 0.f;
-              for (int sp = 0; sp < splits; ++sp)
-                o += __ldcg(args.ws + ((long long)sp * args.M + t) * args.N + f);
-              if (args.residual) o += bf2f(args.residual[(long long)t * args.ldc + f]);
-              args.C[(long long)t * args.ldc + f] = f2bf(o);
-            }
+            if (args.residual) o += bf2f(args.residual[(long long)t * args.ldc + f]);
+            args.C[(long long)t * args.ldc + f] = f2bf(o);
           }
-          if (threadIdx.x == 64) args.counters[tile_a] = 0;  // ready for the next launch
         }
+        if (threadIdx.x == 64) args.counters[tile] = 0;
       }
     }
   }
@@ -370,61 +519,63 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, dim3
     ASTRAEA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  kern<<<grid, kThreads, smem, st>>>(ma, mb, a);
-  ASTRAEA_CHECK_LAUNCH();
+  ASTRAEA_TRY(launch_k(kern, grid, dim3(kThreads), smem, st, ma, mb, a));
   return 0;
 }
 
 constexpr int kColsMaxM = 64;
 
-// Decode path: split count that best fills the SMs (wave quantisation).
-int pick_splits(int tiles, int total_kb, int slots) {
-  int best = 1;
-  double best_eff = 0.0;
-  for (int s = 1; s <= 16; ++s) {
-    if (total_kb / s < 4) break;
-    const long long ctas = (long long)tiles * s;
-    const long long waves = (ctas + slots - 1) / slots;
-    const double eff = (double)ctas / (double)(waves * slots);
-    if (eff > best_eff + 0.02) {
-      best_eff = eff;
-      best = s;
-    }
-  }
-  return best;
-}
-
-
-struct ColsPlan {
-  int bn, tiles, splits, kb_per_split;
+struct SkPlan {
+  int bn, tiles, kbs, grid, maxseg;
+  long long units;
 };
 
-ColsPlan cols_plan(int M, int N, int K) {
-  ColsPlan p;
+SkPlan sk_plan(int M, int N, int K) {
+  SkPlan p;
   p.bn = M <= 16 ? 16 : (M <= 32 ? 32 : 64);
   p.tiles = (N + kBM - 1) / kBM;
-  const int total_kb = (K + kBK - 1) / kBK;
-  const int s = pick_splits(p.tiles, total_kb, 2 * num_sms());
-  p.kb_per_split = (total_kb + s - 1) / s;
-  p.splits = (total_kb + p.kb_per_split - 1) / p.kb_per_split;
+  p.kbs = (K + kBK - 1) / kBK;
+  p.units = (long long)p.tiles * p.kbs;
+  p.grid = (int)std::min<long long>(num_sms(), p.units);
+  p.maxseg = (p.grid + p.tiles - 1) / p.tiles + 1;
   return p;
 }
 
-// Workspace layout for split-K: a fixed counter region shared by every GEMM
-// shape (so GEMMs of different tile counts can reuse one workspace in
-// stream order without clobbering each other's counters), then partials.
+// Workspace layout: a fixed counter region shared by every GEMM shape (so
+// GEMMs of different tile counts reuse one workspace in stream order without
+// clobbering each other's counters), then the fp32 partials.
 constexpr size_t kCounterBytes = 16384 * sizeof(int);
 
-size_t cols_ws_bytes(int M, int N, const ColsPlan& p) {
-  if (p.splits == 1) return 0;
-  return kCounterBytes + (size_t)p.splits * M * N * sizeof(float);
+size_t sk_ws_bytes(int M, const SkPlan& p) {
+  return kCounterBytes + (size_t)p.tiles * p.maxseg * M * kBM * sizeof(float);
+}
+
+template <int BN>
+constexpr int sk_stages() {
+  // ~100 KB: two CTAs fit per SM, so the next GEMM's CTA can become resident
+  // and prefetch its weights (PDL) while this one drains.
+  return (100 * 1024) / (kBM * kBK * 2 + BN * kBK * 2);
+}
+
+template <int BN>
+int launch_sk(const CUtensorMap& mw, const CUtensorMap& mx, const SkArgs& a, cudaStream_t st) {
+  constexpr int S = sk_stages<BN>();
+  auto kern = gemm_streamk_kernel<BN, S>;
+  constexpr size_t smem = 1024 + (size_t)S * (kBM * kBK * 2 + BN * kBK * 2) + (2 * S + 4) * 8 + 16;
+  static bool attr = false;
+  if (!attr) {
+    ASTRAEA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  ASTRAEA_TRY(launch_k(kern, dim3(a.grid), dim3(kThreads), smem, st, mw, mx, a));
+  return 0;
 }
 
 }  // namespace
 
 extern "C" size_t astraea_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K) {
   if (M <= 0 || M > kColsMaxM || N <= 0 || K <= 0) return 0;
-  return cols_ws_bytes(M, N, cols_plan(M, N, K));
+  return sk_ws_bytes(M, sk_plan(M, N, K));
 }
 
 extern "C" int astraea_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, void* C, int32_t ldc,
@@ -436,6 +587,32 @@ extern "C" int astraea_gemm_bf16(const void* A, int32_t lda, const void* W, int3
   if (epilogue == ASTRAEA_EPI_NONE) residual = nullptr;
   if (M == 0) return ASTRAEA_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  CUtensorMap ma, mb;
+  int rc;
+  if (M <= kColsMaxM) {
+    const SkPlan p = sk_plan(M, N, K);
+    if (!ws || ws_bytes < sk_ws_bytes(M, p)) return ASTRAEA_EINVAL;
+    if ((size_t)p.tiles * sizeof(int) > kCounterBytes) return ASTRAEA_EUNSUPPORTED;
+    SkArgs a;
+    a.C = (bf16*)C;
+    a.residual = (const bf16*)residual;
+    a.counters = (int*)ws;
+    a.ws = (float*)((char*)ws + kCounterBytes);
+    a.M = M;
+    a.N = N;
+    a.K = K;
+    a.ldc = ldc;
+    a.tiles = p.tiles;
+    a.kbs = p.kbs;
+    a.grid = p.grid;
+    a.maxseg = p.maxseg;
+    a.units = p.units;
+    if ((rc = make_map(&ma, W, N, K, ldw, kBM))) return rc;
+    if ((rc = make_map(&mb, A, M, K, lda, p.bn))) return rc;
+    if (p.bn == 16) return launch_sk<16>(ma, mb, a, st);
+    if (p.bn == 32) return launch_sk<32>(ma, mb, a, st);
+    return launch_sk<64>(ma, mb, a, st);
+  }
   GemmArgs a;
   a.C = (bf16*)C;
   a.residual = (const bf16*)residual;
@@ -445,26 +622,6 @@ extern "C" int astraea_gemm_bf16(const void* A, int32_t lda, const void* W, int3
   a.N = N;
   a.K = K;
   a.ldc = ldc;
-  CUtensorMap ma, mb;
-  int rc;
-  if (M <= kColsMaxM) {
-    // swap-AB: MMA A = W (128 features), MMA B = activations (bn tokens)
-    const ColsPlan p = cols_plan(M, N, K);
-    const size_t need = cols_ws_bytes(M, N, p);
-    if (need) {
-      if (!ws || ws_bytes < need) return ASTRAEA_EINVAL;
-      if ((size_t)p.tiles * sizeof(int) > kCounterBytes) return ASTRAEA_EUNSUPPORTED;
-      a.counters = (int*)ws;
-      a.ws = (float*)((char*)ws + kCounterBytes);
-    }
-    a.kb_per_split = p.kb_per_split;
-    if ((rc = make_map(&ma, W, N, K, ldw, kBM))) return rc;
-    if ((rc = make_map(&mb, A, M, K, lda, p.bn))) return rc;
-    dim3 grid(p.tiles, 1, p.splits);
-    if (p.bn == 16) return launch<16, 8, kCols>(ma, mb, a, grid, st);
-    if (p.bn == 32) return launch<32, 8, kCols>(ma, mb, a, grid, st);
-    return launch<64, 6, kCols>(ma, mb, a, grid, st);
-  }
   a.kb_per_split = (K + kBK - 1) / kBK;
   const int bn = (N % 256 == 0 && (long long)((M + kBM - 1) / kBM) * (N / 256) >= num_sms()) ? 256 : 128;
   if ((rc = make_map(&ma, A, M, K, lda, kBM))) return rc;

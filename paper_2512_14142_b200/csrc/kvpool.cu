@@ -266,6 +266,8 @@ __global__ void table_build_kernel(const int32_t* __restrict__ ptr, const int32_
                                    int32_t max_blocks, int32_t* __restrict__ table,
                                    int32_t* __restrict__ ctx) {
   const int b = blockIdx.x;
+  pdl_wait();
+  pdl_launch();
   const int r = rows[b];
   const int begin = ptr[r];
   const int n = ptr[r + 1] - begin;
@@ -279,7 +281,7 @@ extern "C" int astraea_block_table_build(const int32_t* ptr, const int32_t* ids,
                                          int32_t* table, int32_t* ctx, void* stream) {
   if (B < 0 || max_blocks <= 0) return ASTRAEA_EINVAL;
   if (B == 0) return ASTRAEA_OK;
-  table_build_kernel<<<B, 128, 0, (cudaStream_t)stream>>>(ptr, ids, rows, ctx_src, max_blocks, table, ctx);
+  ASTRAEA_TRY(launch_k(table_build_kernel, dim3(B), dim3(128), 0, (cudaStream_t)stream, ptr, ids, rows, ctx_src, max_blocks, table, ctx));
   ASTRAEA_CHECK_LAUNCH();
   return ASTRAEA_OK;
 }
@@ -294,6 +296,8 @@ __global__ void __launch_bounds__(256) rope_append_kernel(
     const int32_t* __restrict__ slots, bf16* __restrict__ pool, long long block_bytes_el,
     int layer, int bt, float theta) {
   const int t = blockIdx.x;
+  pdl_wait();
+  pdl_launch();
   const int H = Hq + 2 * Hkv;
   bf16* row = qkv + (long long)t * H * D;
   const float pos = (float)positions[t];
@@ -346,11 +350,11 @@ extern "C" int astraea_rope_kv_append(const astraea_kv_geometry* g, void* pool, 
   const long long bbe = (long long)astraea_kv_block_bytes(g) / 2;
   cudaStream_t st = (cudaStream_t)stream;
   if (g->head_dim == 128)
-    rope_append_kernel<128><<<T, 256, 0, st>>>((bf16*)qkv, Hq, g->num_kv_heads, positions, slots,
-                                               (bf16*)pool, bbe, layer, g->block_tokens, theta);
+    ASTRAEA_TRY(launch_k(rope_append_kernel<128>, dim3(T), dim3(256), 0, st, (bf16*)qkv, (int)Hq, (int)g->num_kv_heads,
+                         positions, slots, (bf16*)pool, bbe, (int)layer, (int)g->block_tokens, theta));
   else
-    rope_append_kernel<64><<<T, 256, 0, st>>>((bf16*)qkv, Hq, g->num_kv_heads, positions, slots,
-                                              (bf16*)pool, bbe, layer, g->block_tokens, theta);
+    ASTRAEA_TRY(launch_k(rope_append_kernel<64>, dim3(T), dim3(256), 0, st, (bf16*)qkv, (int)Hq, (int)g->num_kv_heads,
+                         positions, slots, (bf16*)pool, bbe, (int)layer, (int)g->block_tokens, theta));
   ASTRAEA_CHECK_LAUNCH();
   return ASTRAEA_OK;
 }
@@ -364,6 +368,8 @@ __global__ void decode_advance_kernel(int32_t* __restrict__ step_ctr, int B, con
                                       int max_blocks, int bt, int32_t* __restrict__ tokens,
                                       int32_t* __restrict__ positions, int32_t* __restrict__ slots,
                                       int32_t* __restrict__ ctx, int32_t* __restrict__ hist, int hist_stride) {
+  pdl_wait();
+  pdl_launch();
   const int step = *step_ctr;
   for (int b = threadIdx.x; b < B; b += blockDim.x) {
     if (step < n_gen[b]) {
@@ -394,9 +400,9 @@ extern "C" int astraea_decode_advance(int32_t* step, int32_t B, const int32_t* n
                                       int32_t* slots, int32_t* ctx, int32_t* hist, int32_t hist_stride,
                                       void* stream) {
   if (!step || B <= 0 || B > 1024 || max_blocks <= 0 || bt <= 0) return ASTRAEA_EINVAL;
-  decode_advance_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(step, B, n_gen, base_pos, first_tok, sampled, table,
-                                                             max_blocks, bt, tokens, positions, slots, ctx, hist,
-                                                             hist_stride);
+  ASTRAEA_TRY(launch_k(decode_advance_kernel, dim3(1), dim3(256), 0, (cudaStream_t)stream, step, (int)B, n_gen,
+                       base_pos, first_tok, sampled, table, (int)max_blocks, (int)bt, tokens, positions, slots, ctx,
+                       hist, (int)hist_stride));
   ASTRAEA_CHECK_LAUNCH();
   return ASTRAEA_OK;
 }

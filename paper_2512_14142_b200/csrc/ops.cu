@@ -17,6 +17,8 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const bf16* __restrict__ x
                                                       const bf16* __restrict__ w, bf16* __restrict__ y,
                                                       bf16* __restrict__ resid_out, int dim, float eps) {
   const long long row = blockIdx.x;
+  pdl_wait();
+  pdl_launch();
   const int nvec = dim / 8;
   float v[VPT][8];
   float ss = 0.f;
@@ -68,6 +70,8 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const bf16* __restrict__ x
 }
 
 __global__ void silu_mul_kernel(const bf16* __restrict__ gu, bf16* __restrict__ out, int F, long long total_vec) {
+  pdl_wait();
+  pdl_launch();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total_vec;
        i += (long long)gridDim.x * blockDim.x) {
     const long long t = i / (F / 8);
@@ -88,6 +92,8 @@ __global__ void silu_mul_kernel(const bf16* __restrict__ gu, bf16* __restrict__ 
 __global__ void embedding_kernel(const int32_t* __restrict__ ids, const bf16* __restrict__ table,
                                  bf16* __restrict__ out, int dim) {
   const long long t = blockIdx.x;
+  pdl_wait();
+  pdl_launch();
   const long long id = ids[t];
   for (int i = threadIdx.x; i < dim / 8; i += blockDim.x)
     *reinterpret_cast<uint4*>(out + t * dim + i * 8) =
@@ -97,6 +103,8 @@ __global__ void embedding_kernel(const int32_t* __restrict__ ids, const bf16* __
 __global__ void __launch_bounds__(1024) argmax_kernel(const bf16* __restrict__ logits, int vocab,
                                                       int32_t* __restrict__ out) {
   const long long row = blockIdx.x;
+  pdl_wait();
+  pdl_launch();
   const bf16* lr = logits + row * vocab;
   float best = -FLT_MAX;
   int bidx = 0x7fffffff;
@@ -150,15 +158,16 @@ extern "C" int astraea_rmsnorm(const void* x, const void* r, const void* w, void
   const int nvec = dim / 8;
   const int threads = nvec >= 256 ? 256 : ((nvec + 31) / 32) * 32;
   const int vpt = (nvec + threads - 1) / threads;
+  cudaError_t err = cudaSuccess;
   auto args = [&](auto kern) {
-    kern<<<rows, threads, 0, st>>>((const bf16*)x, (const bf16*)r, (const bf16*)w, (bf16*)y,
-                                   (bf16*)resid_out, dim, eps);
+    err = launch_k(kern, dim3(rows), dim3(threads), 0, st, (const bf16*)x, (const bf16*)r, (const bf16*)w, (bf16*)y,
+                   (bf16*)resid_out, (int)dim, eps);
   };
   if (vpt <= 1) args(rmsnorm_kernel<1>);
   else if (vpt <= 2) args(rmsnorm_kernel<2>);
   else if (vpt <= 4) args(rmsnorm_kernel<4>);
   else args(rmsnorm_kernel<8>);
-  ASTRAEA_CHECK_LAUNCH();
+  ASTRAEA_TRY(err);
   return ASTRAEA_OK;
 }
 
@@ -168,7 +177,8 @@ extern "C" int astraea_silu_mul(const void* gu, void* out, int32_t T, int32_t F,
   const long long total = (long long)T * F / 8;
   long long want = (total + 255) / 256, cap = 8LL * num_sms();
   const int grid = (int)(want < cap ? want : cap);
-  silu_mul_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const bf16*)gu, (bf16*)out, F, total);
+  ASTRAEA_TRY(launch_k(silu_mul_kernel, dim3(grid), dim3(256), 0, (cudaStream_t)stream, (const bf16*)gu, (bf16*)out,
+                       (int)F, total));
   ASTRAEA_CHECK_LAUNCH();
   return ASTRAEA_OK;
 }
@@ -177,7 +187,8 @@ extern "C" int astraea_embedding(const int32_t* ids, const void* table, void* ou
                                  void* stream) {
   if (T < 0 || dim <= 0 || dim % 8) return ASTRAEA_EINVAL;
   if (T == 0) return ASTRAEA_OK;
-  embedding_kernel<<<T, 128, 0, (cudaStream_t)stream>>>(ids, (const bf16*)table, (bf16*)out, dim);
+  ASTRAEA_TRY(launch_k(embedding_kernel, dim3(T), dim3(128), 0, (cudaStream_t)stream, ids, (const bf16*)table,
+                       (bf16*)out, (int)dim));
   ASTRAEA_CHECK_LAUNCH();
   return ASTRAEA_OK;
 }
@@ -185,7 +196,8 @@ extern "C" int astraea_embedding(const int32_t* ids, const void* table, void* ou
 extern "C" int astraea_argmax(const void* logits, int32_t rows, int32_t vocab, int32_t* ids_out, void* stream) {
   if (rows < 0 || vocab <= 0) return ASTRAEA_EINVAL;
   if (rows == 0) return ASTRAEA_OK;
-  argmax_kernel<<<rows, 1024, 0, (cudaStream_t)stream>>>((const bf16*)logits, vocab, ids_out);
+  ASTRAEA_TRY(launch_k(argmax_kernel, dim3(rows), dim3(1024), 0, (cudaStream_t)stream, (const bf16*)logits,
+                       (int)vocab, ids_out));
   ASTRAEA_CHECK_LAUNCH();
   return ASTRAEA_OK;
 }

@@ -119,14 +119,14 @@ def decode_attention(geo, pool, layer, q, q_row_stride, B, num_q_heads, table, c
         ctypes.byref(geo), L.ptr(pool), layer, L.ptr(q), q_row_stride, B, num_q_heads, L.ptr(table),
         table.shape[1], L.ptr(ctx), scale, L.ptr(out), L.ptr(workspace),
         workspace.numel() * workspace.element_size(), _s(stream)), "paged_decode_attention")
-    _count(1 + (decode_splits(B, geo.num_kv_heads, table.shape[1]) > 1))
+    _count()
     return out
 
 
 def decode_workspace(B, num_q_heads, head_dim, max_blocks, device) -> torch.Tensor:
     lib = L.load()
     n = lib.astraea_decode_workspace_bytes(B, num_q_heads, head_dim, max_blocks)
-    return torch.empty(n // 4 + 1, dtype=torch.float32, device=device)
+    return torch.zeros(n // 4 + 1, dtype=torch.float32, device=device)
 
 
 def prefill_attention(geo, pool, layer, q, q_row_stride, cu_q, S, max_q_len, num_q_heads, table, ctx,
