@@ -68,8 +68,14 @@ def peaks():
 def build_workload(args, rank, world):
     from paper_2512_14142_b200 import host
     import scenarios
-    cfg = host.WorkloadConfig(seed=0, qps=args.qps * world, duration=1e6)
-    full = host.generate(cfg)[: args.requests * world]
+    need = args.requests * world
+    duration = 2.0 * need / (args.qps * world) + 60.0
+    while True:  # the first n arrivals do not depend on the horizon once it covers them
+        full = host.generate(host.WorkloadConfig(seed=0, qps=args.qps * world, duration=duration))
+        if len(full) >= need:
+            break
+        duration *= 2
+    full = full[:need]
     full.sort(key=lambda r: (r.arrival_time, r.id))
     shard = full[rank::world]
     pred = scenarios.b200_like_predictor(host)

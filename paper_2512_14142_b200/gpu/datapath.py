@@ -34,7 +34,6 @@ import numpy as np
 import torch
 
 from ..host.errors import ProtocolError
-from ..host.policies import CacheLocation
 from ..host.trace import segment_token_ids
 from . import lib as L
 from . import ops
@@ -72,6 +71,12 @@ class ReqDev:
 
 def _blocks_for(tokens: int) -> int:
     return (tokens + BT - 1) // BT
+
+
+def _loc(location) -> str:
+    """Cache location by value, so states of the host mirror *and* of the
+    unmodified reference package (its own CacheLocation enum) both work."""
+    return location.value
 
 
 class KvDataPath:
@@ -204,7 +209,7 @@ class KvDataPath:
         rd = self.reqs.pop(state.spec.id, None)
         if rd is None:
             return
-        if where is CacheLocation.GPU:
+        if _loc(where) == "gpu":
             self._free_blocks(rd)
         if rd.slot is not None:
             self._defer(rd.swap_ev[1], rd.slot)
@@ -237,12 +242,13 @@ class KvDataPath:
             rd = self._rd(st)
             ctx_before = st.context_before_current
             ctx_after = st.context_after(m.segment_index)
-            if m.prior_location is CacheLocation.GPU:
+            prior = _loc(m.prior_location)
+            if prior == "gpu":
                 if rd.tokens != ctx_before or rd.hist_len != ctx_before:
                     raise ProtocolError(f"{rid}: resident KV {rd.tokens} != context {ctx_before}")
                 start = ctx_before
                 recompute = False
-            elif m.prior_location in (CacheLocation.NONE, CacheLocation.DROPPED):
+            elif prior in ("none", "dropped"):
                 if rd.blocks:
                     raise ProtocolError(f"{rid}: {m.prior_location} request still holds blocks")
                 start = 0
@@ -417,7 +423,7 @@ class KvDataPath:
         for st in states:
             rd = self.reqs.get(st.spec.id)
             nb = len(rd.blocks) if rd else 0
-            want = _blocks_for(st.kv_tokens) if st.cache_location is CacheLocation.GPU else 0
+            want = _blocks_for(st.kv_tokens) if _loc(st.cache_location) == "gpu" else 0
             if nb != want:
                 raise ProtocolError(f"device blocks drifted for {st.spec.id}: {nb} held, {want} expected")
             held += nb
