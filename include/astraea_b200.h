@@ -189,12 +189,47 @@ ASTRAEA_API int astraea_paged_prefill_attention(const astraea_kv_geometry* g, co
  * NULL when astraea_gemm_workspace_bytes() returns 0; otherwise it must be
  * zero-filled once before first use (its arrival counters are reset by the
  * kernel itself) and not shared by concurrently running GEMMs. */
-enum { ASTRAEA_EPI_NONE = 0, ASTRAEA_EPI_RESIDUAL = 1 };
+enum { ASTRAEA_EPI_NONE = 0, ASTRAEA_EPI_RESIDUAL = 1, ASTRAEA_EPI_SILU = 2, ASTRAEA_EPI_QKV_ROPE = 3 };
 ASTRAEA_API size_t astraea_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K);
 ASTRAEA_API int astraea_gemm_bf16(const void* A_dev, int32_t lda, const void* W_dev, int32_t ldw,
                       void* C_dev, int32_t ldc, int32_t M, int32_t N, int32_t K,
                       const void* residual_dev, int32_t epilogue, void* workspace_dev,
                       size_t workspace_bytes, void* stream);
+
+/* Fused epilogue programs of the Llama block (the small per-layer kernels
+ * never run as separate launches on the decode path):
+ *   NONE       C = acc
+ *   RESIDUAL   C = acc + residual (may alias C); if ssq_out_dev != NULL also
+ *              writes ssq_out[ceil(N/128)][M]: per-128-column sums of squares
+ *              of the bf16 output -- the statistics of the next RMSNorm
+ *   SILU       W rows interleaved [64 gate | 64 up] per 128 rows (N = 2F):
+ *              C[M][F] = silu(gate) * up
+ *   QKV_ROPE   N = (Hq + 2 Hkv) * head_dim: RoPE (theta, NeoX half split) on
+ *              q and k at positions[t]; C[M][Hq*D] receives q; k and v rows
+ *              are written to the pool at slots[t] (slot < 0: skipped)
+ * and for any program, input RMS scaling when ssq_in_dev != NULL:
+ *   acc[t][:] *= rsqrt(sum_p ssq_in[p][t] / rms_dim + rms_eps)
+ * (the norm weight is folded into W by the caller). */
+typedef struct {
+  int32_t kind;
+  const void* residual_dev;
+  float* ssq_out_dev;
+  const float* ssq_in_dev;
+  int32_t ssq_in_parts;
+  int32_t rms_dim;
+  float rms_eps;
+  void* pool_dev;
+  astraea_kv_geometry geo;
+  int32_t layer;
+  int32_t num_q_heads;
+  const int32_t* positions_dev;
+  const int32_t* slots_dev;
+  float rope_theta;
+} astraea_epilogue;
+ASTRAEA_API int astraea_gemm_bf16_ex(const void* A_dev, int32_t lda, const void* W_dev, int32_t ldw,
+                         void* C_dev, int32_t ldc, int32_t M, int32_t N, int32_t K,
+                         const astraea_epilogue* epilogue, void* workspace_dev,
+                         size_t workspace_bytes, void* stream);
 
 /* ---- K8: small fused ops --------------------------------------------------------------------------- */
 /* y = rmsnorm(x + r) * w ; if resid_out_dev != NULL it receives x + r. r may be NULL. */
@@ -202,9 +237,10 @@ ASTRAEA_API int astraea_rmsnorm(const void* x_dev, const void* r_dev, const void
                     void* resid_out_dev, int32_t rows, int32_t dim, float eps, void* stream);
 /* out[T][F] = silu(gu[T][0:F]) * gu[T][F:2F] */
 ASTRAEA_API int astraea_silu_mul(const void* gu_dev, void* out_dev, int32_t T, int32_t F, void* stream);
-/* out[T][dim] = table[ids[T]][dim] */
+/* out[T][dim] = table[ids[T]][dim]; if ssq_out_dev != NULL, ssq_out[t] = sum of
+ * squares of the row (one-part RMS statistics for the first layer's norm). */
 ASTRAEA_API int astraea_embedding(const int32_t* ids_dev, const void* table_dev, void* out_dev, int32_t T,
-                      int32_t dim, void* stream);
+                      int32_t dim, float* ssq_out_dev, void* stream);
 /* ids_out[r] = argmax_j logits[r][j] (lowest index on ties); logits bf16 [rows][vocab]. */
 ASTRAEA_API int astraea_argmax(const void* logits_dev, int32_t rows, int32_t vocab, int32_t* ids_out_dev,
                    void* stream);

@@ -7,8 +7,11 @@ sequence, i.e. *without* paging, so the device's paged KV, block tables,
 swap and recompute are all checked against a layout-free computation.
 
 ``bf16_points=True`` rounds tensors to bf16 at the points where the device
-materialises bf16 (every op output, the residual stream), which removes the
-storage-precision part of the difference and leaves accumulation order.
+materialises bf16 (projection outputs, RoPE outputs, SiLU, the residual
+stream; the normalised activations are never materialised on the device --
+the norm is applied to the fp32 accumulators -- so they are not rounded
+here either), which removes the storage-precision part of the difference
+and leaves accumulation order.
 """
 
 import torch
@@ -41,7 +44,7 @@ def forward(w, cfg, ids, bf16_points=True):
     x = w["embed"][torch.as_tensor(ids, dtype=torch.long)].float()
     mask = torch.triu(torch.ones(T, T, dtype=torch.bool), 1)
     for lw in w["layers"]:
-        h = r(rmsnorm(x, lw["attn_norm"].float(), cfg.eps))
+        h = rmsnorm(x, lw["attn_norm"].float(), cfg.eps)
         qkv = r(h @ lw["wqkv"].float().T)
         q = qkv[:, : Hq * D].view(T, Hq, D)
         k = qkv[:, Hq * D: (Hq + Hkv) * D].view(T, Hkv, D)
@@ -54,12 +57,12 @@ def forward(w, cfg, ids, bf16_points=True):
         s = s.masked_fill(mask.unsqueeze(0), float("-inf"))
         a = r(torch.einsum("hqk,khd->qhd", torch.softmax(s, -1), vv).reshape(T, Hq * D))
         x = r(a @ lw["wo"].float().T + x)
-        h = r(rmsnorm(x, lw["mlp_norm"].float(), cfg.eps))
+        h = rmsnorm(x, lw["mlp_norm"].float(), cfg.eps)
         gu = r(h @ lw["wgu"].float().T)
         g, u = gu[:, : cfg.ffn], gu[:, cfg.ffn:]
         m = r(r(torch.nn.functional.silu(g)) * u)
         x = r(m @ lw["wdown"].float().T + x)
-    h = r(rmsnorm(x, w["final_norm"].float(), cfg.eps))
+    h = rmsnorm(x, w["final_norm"].float(), cfg.eps)
     return h @ w["lm_head"].float().T
 
 

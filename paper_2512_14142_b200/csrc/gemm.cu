@@ -1,28 +1,39 @@
-// K6 / K9: bf16 GEMM on 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+// K6 / K9: bf16 GEMM on 5th-generation tensor cores (tcgen05 + TMEM + TMA),
+// with the Llama block's elementwise work fused into the epilogue.
 //
-//   C[M][N] = A[M][K] . W[N][K]^T  (+ residual)
+//   C[M][N] = epilogue( A[M][K] . W[N][K]^T )
 //
 // These are the dense projections of the recompute-on-resume prefill and of
 // every decode step -- the work the reference reduces to the profile lookup
 // prefill_seconds(n_in + extra) and n_gen * seconds_per_token
 // (pkg/src/agentsched/predictor.py:47-66, simulator.py:329-337).
 //
-// Kernel anatomy (one output tile per CTA, 192 threads):
+// Kernel anatomy (192 threads):
 //   warp 0      TMA producer: 128B-swizzled A/B tiles into a smem ring
-//               (cp.async.bulk.tensor.2d, mbarrier complete_tx);
+//               (cp.async.bulk.tensor.2d, mbarrier complete_tx); weight tiles
+//               of the first stages are fetched before griddepcontrol.wait,
+//               i.e. while the previous kernel drains (PDL);
 //   warp 1      allocates TMEM; one elected lane issues tcgen05.mma
 //               (kind::f16, M=128, fp32 accumulators in TMEM) and commits
 //               each stage back to the producer with tcgen05.commit;
-//   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> global.
+//   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> fused epilogue.
 //
-// Two operand orientations:
-//   kRows  (prefill, M large): MMA M axis = rows of A (tokens), N axis =
-//          rows of W; bf16 output (+ residual) stored directly.
-//   kCols  (decode, M <= 64): MMA M axis = rows of W (128 output features),
-//          N axis = the M tokens padded to 16/32/64 ("swap AB"), with
-//          split-K across CTAs so the weight stream covers all SMs; the
-//          last CTA of each tile reduces the fp32 partials in split order
-//          (deterministic) and applies the bf16 (+ residual) epilogue.
+// Orientations:
+//   kRows  (prefill, M > 64): MMA M axis = 128 rows of A (tokens), N axis =
+//          128/256 rows of W, one output tile per CTA.
+//   stream-K (decode, M <= 64): MMA M axis = 128 rows of W (output features),
+//          N axis = the M tokens padded to 16/32/64 ("swap AB"); persistent,
+//          one CTA per SM, deterministic split-tile fix-up.
+//
+// Epilogue programs (astraea_epilogue.kind):
+//   NONE       C = acc
+//   RESIDUAL   C = acc + residual (may alias C); optionally emits per-128-
+//              column sums of squares of the bf16 output (the next RMSNorm's
+//              statistics, so the norm itself never runs as a kernel)
+//   SILU       W rows interleaved as [64 gate | 64 up] per 128: C = silu(g)*u
+//   QKV_ROPE   N = (Hq + 2 Hkv) D: RoPE on q and k, q -> C, k/v -> KV pool slots
+// plus, for any program, input RMS scaling: acc[t][:] *= rsqrt(ssq_t/d + eps)
+// with the norm weight folded into W offline (x*w @ W^T == x @ (W diag w)^T).
 #include <cuda.h>
 
 #include <algorithm>
@@ -108,26 +119,77 @@ __host__ __device__ constexpr uint32_t instr_desc(int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
 }
 
-enum Orient { kRows = 0, kCols = 1 };
+__device__ __forceinline__ float round_bf(float x) { return bf2f(f2bf(x)); }
+
+__device__ __forceinline__ float silu_rounded(float g) {
+  // silu(g) is materialised in bf16 by the reference formulation
+  return round_bf(g / (1.f + __expf(-g)));
+}
+
+// ---- epilogue program --------------------------------------------------------------
+
+struct Epi {
+  int kind;
+  const bf16* residual;
+  float* ssq_out;          // [ceil(N/128)][M]
+  const float* ssq_in;     // [parts][M]
+  int ssq_parts;
+  int rms_dim;
+  float eps;
+  bf16* pool;
+  long long block_el;
+  int layer, Hq, Hkv, D, bt;
+  const int32_t* pos;
+  const int32_t* slots;
+  float theta;
+};
+
+__device__ __forceinline__ float rms_scale(const Epi& e, int M, int t) {
+  float s = 0.f;
+  for (int p = 0; p < e.ssq_parts; ++p) s += e.ssq_in[(long long)p * M + t];
+  return rsqrtf(s / (float)e.rms_dim + e.eps);
+}
+
+__device__ __forceinline__ float rope_inv_freq(const Epi& e, int i) {
+  return 1.0f / powf(e.theta, (float)(2 * i) / (float)e.D);
+}
+
+// Destination of a rotated/plain head element in QKV_ROPE: q -> C, k/v -> pool.
+__device__ __forceinline__ void qkv_store(const Epi& e, bf16* C, int ldc, int t, int head, int hrow, float y) {
+  if (head < e.Hq) {
+    C[(long long)t * ldc + head * e.D + hrow] = f2bf(y);
+    return;
+  }
+  const int slot = e.slots[t];
+  if (slot < 0) return;
+  const int kv = head < e.Hq + e.Hkv ? 0 : 1;
+  const int h = head - e.Hq - kv * e.Hkv;
+  const int blk = slot / e.bt, off = slot % e.bt;
+  bf16* base = e.pool + (long long)blk * e.block_el + ((long long)(e.layer * 2 + kv) * e.Hkv + h) * e.bt * e.D;
+  base[(long long)off * e.D + hrow] = f2bf(y);
+}
+
+enum { EPI_NONE = 0, EPI_RESIDUAL = 1, EPI_SILU = 2, EPI_QKV_ROPE = 3 };
 
 struct GemmArgs {
   bf16* C;
-  const bf16* residual;
-  float* ws;          // kCols split-K: fp32 [splits][M][N] partials
-  int* counters;      // kCols split-K: per-tile arrival counters (zero between launches)
   int M, N, K, ldc;
-  int kb_per_split;   // K blocks per CTA (split-K)
+  Epi epi;
 };
 
-// BN: MMA N (tile width along the N axis of the MMA).
-template <int BN, int STAGES, int ORIENT>
+// ---------------------------------------------------------------------------
+// kRows (prefill): one 128 x BN output tile per CTA. Epilogue thread = one
+// token row; columns are processed in 128-column groups (4 TMEM chunks of
+// 32), pairing chunk c with chunk c + 2 (SILU, RoPE at D=128) or c + 1 (RoPE
+// at D=64) so every rotation / gate-up pair is register local.
+// ---------------------------------------------------------------------------
+template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                const __grid_constant__ GemmArgs args) {
-  // map_a feeds the MMA "A" (M axis, 128 rows), map_b the MMA "B" (BN rows).
+    gemm_rows_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                     const __grid_constant__ GemmArgs args) {
   constexpr int A_BYTES = kBM * kBK * 2;
   constexpr int B_BYTES = BN * kBK * 2;
-  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  constexpr uint32_t TMEM_COLS = BN;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;
@@ -138,13 +200,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile_a = blockIdx.x;   // along the MMA M axis (128)
-  const int tile_b = blockIdx.y;   // along the MMA N axis (BN)
-  const int split = blockIdx.z;
-  const int total_kb = (args.K + kBK - 1) / kBK;
-  const int kb0 = split * args.kb_per_split;
-  const int kb1 = min(total_kb, kb0 + args.kb_per_split);
-  const int nkb = kb1 - kb0;
+  const int tile_a = blockIdx.x;   // tokens (128)
+  const int tile_b = blockIdx.y;   // output columns (BN)
+  const int nkb = (args.K + kBK - 1) / kBK;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
@@ -165,22 +223,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_launch();
   if (warp == 0) {
     if (lane == 0) {
-      // Weights (map_b) do not depend on the previous kernel: prefetch the
-      // first stages before the grid-dependency wait.
       const int pre = min(nkb, STAGES);
-      for (int i = 0; i < pre; ++i) {
+      for (int i = 0; i < pre; ++i) {  // weights first, before the dependency wait
         mbar_arrive_expect_tx(&full[i], A_BYTES + B_BYTES);
-        tma_load_2d(sb + i * B_BYTES, &map_b, &full[i], (kb0 + i) * kBK, tile_b * BN);
+        tma_load_2d(sb + i * B_BYTES, &map_b, &full[i], i * kBK, tile_b * BN);
       }
       pdl_wait();
-      for (int i = 0; i < pre; ++i) tma_load_2d(sa + i * A_BYTES, &map_a, &full[i], (kb0 + i) * kBK, tile_a * kBM);
+      for (int i = 0; i < pre; ++i) tma_load_2d(sa + i * A_BYTES, &map_a, &full[i], i * kBK, tile_a * kBM);
       for (int i = pre; i < nkb; ++i) {
         const int s = i % STAGES;
         mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
         mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
-        const int kc = (kb0 + i) * kBK;
-        tma_load_2d(sa + s * A_BYTES, &map_a, &full[s], kc, tile_a * kBM);
-        tma_load_2d(sb + s * B_BYTES, &map_b, &full[s], kc, tile_b * BN);
+        tma_load_2d(sa + s * A_BYTES, &map_a, &full[s], i * kBK, tile_a * kBM);
+        tma_load_2d(sb + s * B_BYTES, &map_b, &full[s], i * kBK, tile_b * BN);
       }
     }
   } else if (warp == 1) {
@@ -194,56 +249,105 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t da = smem_desc_sw128(sa + s * A_BYTES);
         const uint64_t db = smem_desc_sw128(sb + s * B_BYTES);
 #pragma unroll
-        for (int k = 0; k < kBK / 16; ++k) {
-          // advance 16 bf16 = 32 bytes along K inside the swizzle atom (>>4 -> +2)
-          mma_bf16(tmem, da + 2 * k, db + 2 * k, idesc, (i | k) != 0);
-        }
+        for (int k = 0; k < kBK / 16; ++k) mma_bf16(tmem, da + 2 * k, db + 2 * k, idesc, (i | k) != 0);
         mma_commit(&empty[s]);
         if (i == nkb - 1) mma_commit(done);
       }
       __syncwarp();
     }
-    if (nkb == 0 && lane == 0) mbar_arrive(done);
   } else {
-    // epilogue: warps 2..5 -> TMEM lane quarter (warp % 4)
     pdl_wait();
+    const Epi& e = args.epi;
     const int quarter = warp & 3;
+    const int m = tile_a * kBM + quarter * 32 + lane;
+    const bool mok = m < args.M;
+    const float rs = (e.ssq_in && mok) ? rms_scale(e, args.M, m) : 1.f;
     mbar_wait(done, 0);
     tc_fence_after();
-    const int row_in_tile = quarter * 32 + lane;
     const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
-    if constexpr (ORIENT == kRows) {
-      const int m = tile_a * kBM + row_in_tile;
+    bf16* crow = args.C + (long long)m * args.ldc;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        float v[32];
-        tmem_ld32(lane_addr + c0, v);
-        const int n0 = tile_b * BN + c0;
-        if (m < args.M && nkb > 0) {
-          bf16* dst = args.C + (long long)m * args.ldc + n0;
-          if (n0 + 32 <= args.N) {
+    for (int g = 0; g < BN / 128; ++g) {
+      const int n_group = tile_b * BN + g * 128;    // first output column of the 128-group
+      if (e.kind == EPI_SILU || e.kind == EPI_QKV_ROPE) {
+        const int pair = (e.kind == EPI_SILU || e.D == 128) ? 2 : 1;   // chunk distance of a pair
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          if ((c / pair) % 2) continue;                 // c is the low half of its pair
+          float lo[32], hi[32];
+          tmem_ld32(lane_addr + g * 128 + c * 32, lo);
+          tmem_ld32(lane_addr + g * 128 + (c + pair) * 32, hi);
+          if (!mok || n_group >= args.N) continue;
+          if (e.kind == EPI_SILU) {
+            const int f0 = (n_group / 128) * 64 + c * 32;   // output feature of lo[0]
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int j = 0; j < 32; j += 8) {
               float o[8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) o[e] = v[q * 8 + e];
-              if (args.residual) {
-                float r[8];
-                unpack8(*reinterpret_cast<const uint4*>(args.residual + (long long)m * args.ldc + n0 + q * 8), r);
-#pragma unroll
-                for (int e = 0; e < 8; ++e) o[e] += r[e];
-              }
-              *reinterpret_cast<uint4*>(dst + q * 8) = pack8(o);
+              for (int q = 0; q < 8; ++q)
+                o[q] = silu_rounded(round_bf(lo[j + q] * rs)) * round_bf(hi[j + q] * rs);
+              *reinterpret_cast<uint4*>(crow + f0 + j) = pack8(o);
             }
           } else {
-            for (int e = 0; e < 32 && n0 + e < args.N; ++e) {
-              float o = v[e];
-              if (args.residual) o += bf2f(args.residual[(long long)m * args.ldc + n0 + e]);
-              dst[e] = f2bf(o);
+            const float pos = (float)e.pos[m];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int col = n_group + c * 32 + j;        // column of the low element
+              const int head = col / e.D, hrow = col % e.D;  // hrow < D/2
+              const float x0 = round_bf(lo[j] * rs), x1 = round_bf(hi[j] * rs);
+              if (head < e.Hq + e.Hkv) {
+                float sn, cs;
+                sincosf(pos * rope_inv_freq(e, hrow), &sn, &cs);
+                qkv_store(e, args.C, args.ldc, m, head, hrow, x0 * cs - x1 * sn);
+                qkv_store(e, args.C, args.ldc, m, head, hrow + e.D / 2, x1 * cs + x0 * sn);
+              } else {
+                qkv_store(e, args.C, args.ldc, m, head, hrow, x0);
+                qkv_store(e, args.C, args.ldc, m, head, hrow + e.D / 2, x1);
+              }
             }
           }
         }
+        continue;
       }
+      float ssq = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        float v[32];
+        tmem_ld32(lane_addr + g * 128 + c * 32, v);
+        const int n0 = n_group + c * 32;
+        if (!mok || n0 >= args.N) continue;
+        bf16* dst = crow + n0;
+        const bf16* res = e.kind == EPI_RESIDUAL ? e.residual + (long long)m * args.ldc + n0 : nullptr;
+        if (n0 + 32 <= args.N) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float o[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) o[k] = v[q * 8 + k] * rs;
+            if (res) {
+              float r[8];
+              unpack8(*reinterpret_cast<const uint4*>(res + q * 8), r);
+#pragma unroll
+              for (int k = 0; k < 8; ++k) o[k] += r[k];
+            }
+            const uint4 packed = pack8(o);
+            *reinterpret_cast<uint4*>(dst + q * 8) = packed;
+            float ob[8];
+            unpack8(packed, ob);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) ssq += ob[k] * ob[k];
+          }
+        } else {
+          for (int k = 0; k < 32 && n0 + k < args.N; ++k) {
+            float o = v[k] * rs;
+            if (res) o += bf2f(res[k]);
+            const bf16 ob = f2bf(o);
+            dst[k] = ob;
+            ssq += bf2f(ob) * bf2f(ob);
+          }
+        }
+      }
+      if (e.ssq_out && mok && n_group < args.N) e.ssq_out[(long long)(n_group / 128) * args.M + m] = ssq;
     }
   }
   tc_fence_before();
@@ -257,26 +361,108 @@ __global__ void __launch_bounds__(kThreads, 1)
 // MMA A = W rows (128 output features per tile), MMA B = the M <= 64 tokens
 // (BN = 16/32/64). The tiles x k-blocks work units are split evenly over one
 // CTA per SM, so every SM streams the same number of weight bytes (the
-// roofline of a decode step is the weight stream). A CTA walks its units
-// in order: the TMA ring runs continuously across tile boundaries, the MMA
-// warp accumulates each tile *segment* into one of two TMEM accumulators,
-// and the epilogue drains the other. Segments that cover a whole tile are
-// written directly; split tiles are fixed up deterministically -- each
-// segment stores an fp32 partial, the last to arrive sums them in segment
-// order and applies the bf16 (+ residual) epilogue.
+// roofline of a decode step is the weight stream). A CTA walks its units in
+// order: the TMA ring runs continuously across tile boundaries, the MMA warp
+// accumulates each tile *segment* into one of two TMEM accumulators, and the
+// epilogue drains the other. Segments covering a whole tile finish directly;
+// split tiles are fixed up deterministically -- each segment stores an fp32
+// partial, the last to arrive sums them in segment order and finishes.
+// Epilogue thread = one output feature of the tile, all M tokens; pairs that
+// straddle warps (RoPE, gate/up) are exchanged through shared memory.
 // ---------------------------------------------------------------------------
 struct SkArgs {
   bf16* C;
-  const bf16* residual;
   float* ws;        // [tiles][maxseg][M][128] partials
   int* counters;    // [tiles] arrival counters, zero between launches
   int M, N, K, ldc;
   int tiles, kbs, grid, maxseg;
   long long units;
+  Epi epi;
 };
 
 __device__ __forceinline__ int sk_owner(long long u, long long units, int grid) {
   return (int)(((u + 1) * grid - 1) / units);
+}
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// Finish one 128-feature tile: thread `row` holds v[t] (t < M) of feature
+// tile*128 + row. All 128 epilogue threads call this together.
+template <int BN>
+__device__ __forceinline__ void sk_finish(const SkArgs& a, int tile, int row, float* v, const float* rs,
+                                          bf16* xch, float* red) {
+  const Epi& e = a.epi;
+  const int M = a.M;
+  const int f = tile * kBM + row;
+  const bool fok = f < a.N;
+  if (e.ssq_in) {
+#pragma unroll
+    for (int t = 0; t < BN; ++t) v[t] *= rs[t];
+  }
+  if (e.kind == EPI_NONE || e.kind == EPI_RESIDUAL) {
+    float sq[BN];
+#pragma unroll
+    for (int t = 0; t < BN; ++t) {
+      sq[t] = 0.f;
+      if (t < M && fok) {
+        float o = v[t];
+        if (e.kind == EPI_RESIDUAL) o += bf2f(e.residual[(long long)t * a.ldc + f]);
+        const bf16 ob = f2bf(o);
+        a.C[(long long)t * a.ldc + f] = ob;
+        sq[t] = bf2f(ob) * bf2f(ob);
+      }
+    }
+    if (e.ssq_out) {
+      const int q = row >> 5, lane = row & 31;
+#pragma unroll
+      for (int t = 0; t < BN; ++t) {
+        const float s = warp_sum(sq[t]);
+        if (lane == 0) red[q * BN + t] = s;
+      }
+      epi_bar();
+      if (row < M) e.ssq_out[(long long)tile * M + row] = red[row] + red[BN + row] + red[2 * BN + row] + red[3 * BN + row];
+      epi_bar();
+    }
+    return;
+  }
+  // pair exchange through shared memory (values rounded to bf16, as the
+  // unfused formulation materialises them)
+#pragma unroll
+  for (int t = 0; t < BN; ++t) xch[t * kBM + row] = f2bf(v[t]);
+  epi_bar();
+  if (e.kind == EPI_SILU) {
+    if (row >= 64) {
+      const int out_f = tile * 64 + (row - 64);
+      if (fok) {
+#pragma unroll
+        for (int t = 0; t < BN; ++t)
+          if (t < M)
+            a.C[(long long)t * a.ldc + out_f] = f2bf(silu_rounded(bf2f(xch[t * kBM + row - 64])) * bf2f(xch[t * kBM + row]));
+      }
+    }
+  } else {  // QKV_ROPE
+    const int head = f / e.D, hrow = f % e.D, half = e.D / 2;
+    const int partner = row ^ half;
+    const bool rot = head < e.Hq + e.Hkv;
+    float inv = 0.f;
+    if (rot) inv = rope_inv_freq(e, hrow % half);
+    if (fok) {
+#pragma unroll 4
+      for (int t = 0; t < BN; ++t) {
+        if (t >= M) break;
+        const float x = bf2f(xch[t * kBM + row]);
+        float y = x;
+        if (rot) {
+          const float xp = bf2f(xch[t * kBM + partner]);
+          float sn, cs;
+          sincosf((float)e.pos[t] * inv, &sn, &cs);
+          y = hrow < half ? x * cs - xp * sn : x * cs + xp * sn;
+        }
+        qkv_store(e, a.C, a.ldc, t, head, hrow, y);
+      }
+    }
+  }
+  epi_bar();
 }
 
 template <int BN, int STAGES>
@@ -295,6 +481,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  bf16* xch = reinterpret_cast<bf16*>(tmem_slot + 4);        // [BN][128]
+  float* red = reinterpret_cast<float*>(xch + BN * kBM);     // [4][BN]
+  float* rs = red + 4 * BN;                                  // [BN]
   __shared__ int s_last;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -381,6 +570,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int quarter = warp & 3;
     const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
     const int row = quarter * 32 + lane;  // feature within the tile
+    if (args.epi.ssq_in) {
+      if (row < args.M) rs[row] = rms_scale(args.epi, args.M, row);
+      epi_bar();
+    }
     int seg = 0;
     for (long long u = u0; u < u1; ++seg) {
       const long long tile = u / KB;
@@ -396,17 +589,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[buf]);
-      const int f = (int)tile * kBM + row;
-      const bool fok = f < args.N;
       if (whole) {
-#pragma unroll
-        for (int t = 0; t < BN; ++t) {
-          if (t < args.M && fok) {
-            float o = v[t];
-            if (args.residual) o += bf2f(args.residual[(long long)t * args.ldc + f]);
-            args.C[(long long)t * args.ldc + f] = f2bf(o);
-          }
-        }
+        sk_finish<BN>(args, (int)tile, row, v, rs, xch, red);
         continue;
       }
       const long long first_u = tile * KB;
@@ -418,21 +602,21 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int t = 0; t < BN; ++t)
         if (t < args.M) __stcg(part + (long long)t * kBM + row, v[t]);
       __threadfence();
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      epi_bar();
       if (threadIdx.x == 64) s_last = atomicAdd(args.counters + tile, 1) == nseg - 1;
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      epi_bar();
       if (s_last) {
         __threadfence();
         const float* base = args.ws + (tile * args.maxseg * (long long)args.M) * kBM + row;
-        for (int t = 0; t < args.M; ++t) {
+#pragma unroll
+        for (int t = 0; t < BN; ++t) {
           float o = 0.f;
-          for (int sg = 0; sg < nseg; ++sg) o += __ldcg(base + ((long long)sg * args.M + t) * kBM);
-          if (fok) {
-            if (args.residual) o += bf2f(args.residual[(long long)t * args.ldc + f]);
-            args.C[(long long)t * args.ldc + f] = f2bf(o);
-          }
+          if (t < args.M)
+            for (int sg = 0; sg < nseg; ++sg) o += __ldcg(base + ((long long)sg * args.M + t) * kBM);
+          v[t] = o;
         }
         if (threadIdx.x == 64) args.counters[tile] = 0;
+        sk_finish<BN>(args, (int)tile, row, v, rs, xch, red);
       }
     }
   }
@@ -506,14 +690,9 @@ int make_map(CUtensorMap* out, const void* ptr, long long rows, long long cols, 
 }
 
 template <int BN, int STAGES>
-constexpr size_t smem_bytes() {
-  return 1024 + (size_t)STAGES * (kBM * kBK * 2 + BN * kBK * 2) + (2 * STAGES + 1) * 8 + 16;
-}
-
-template <int BN, int STAGES, int ORIENT>
-int launch(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, dim3 grid, cudaStream_t st) {
-  auto kern = gemm_kernel<BN, STAGES, ORIENT>;
-  constexpr size_t smem = smem_bytes<BN, STAGES>();
+int launch_rows(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, dim3 grid, cudaStream_t st) {
+  auto kern = gemm_rows_kernel<BN, STAGES>;
+  constexpr size_t smem = 1024 + (size_t)STAGES * (kBM * kBK * 2 + BN * kBK * 2) + (2 * STAGES + 1) * 8 + 16;
   static bool attr = false;
   if (!attr) {
     ASTRAEA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -550,24 +729,64 @@ size_t sk_ws_bytes(int M, const SkPlan& p) {
   return kCounterBytes + (size_t)p.tiles * p.maxseg * M * kBM * sizeof(float);
 }
 
+// Two CTAs fit per SM (~110 KB each), so the next GEMM's CTA becomes resident
+// and prefetches its weights (PDL) while this one drains.
+template <int BN>
+constexpr size_t sk_extra_bytes() {
+  return (size_t)BN * kBM * 2 + 5 * BN * sizeof(float) + 64;
+}
 template <int BN>
 constexpr int sk_stages() {
-  // ~100 KB: two CTAs fit per SM, so the next GEMM's CTA can become resident
-  // and prefetch its weights (PDL) while this one drains.
-  return (100 * 1024) / (kBM * kBK * 2 + BN * kBK * 2);
+  return (int)((104 * 1024 - sk_extra_bytes<BN>()) / (kBM * kBK * 2 + BN * kBK * 2));
 }
 
 template <int BN>
 int launch_sk(const CUtensorMap& mw, const CUtensorMap& mx, const SkArgs& a, cudaStream_t st) {
   constexpr int S = sk_stages<BN>();
   auto kern = gemm_streamk_kernel<BN, S>;
-  constexpr size_t smem = 1024 + (size_t)S * (kBM * kBK * 2 + BN * kBK * 2) + (2 * S + 4) * 8 + 16;
+  constexpr size_t smem = 1024 + (size_t)S * (kBM * kBK * 2 + BN * kBK * 2) + (2 * S + 4) * 8 + 16 +
+                          sk_extra_bytes<BN>();
   static bool attr = false;
   if (!attr) {
     ASTRAEA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   ASTRAEA_TRY(launch_k(kern, dim3(a.grid), dim3(kThreads), smem, st, mw, mx, a));
+  return 0;
+}
+
+int to_epi(const astraea_epilogue* in, int N, Epi* e) {
+  *e = Epi{};
+  if (!in) return 0;
+  e->kind = in->kind;
+  if (in->kind < EPI_NONE || in->kind > EPI_QKV_ROPE) return ASTRAEA_EINVAL;
+  e->residual = (const bf16*)in->residual_dev;
+  e->ssq_out = in->ssq_out_dev;
+  e->ssq_in = in->ssq_in_dev;
+  e->ssq_parts = in->ssq_in_parts;
+  e->rms_dim = in->rms_dim;
+  e->eps = in->rms_eps;
+  if (e->kind == EPI_RESIDUAL && !e->residual) return ASTRAEA_EINVAL;
+  if (e->ssq_in && (e->ssq_parts <= 0 || e->rms_dim <= 0)) return ASTRAEA_EINVAL;
+  if (e->kind != EPI_RESIDUAL && e->kind != EPI_NONE && e->ssq_out) return ASTRAEA_EINVAL;
+  if (e->kind == EPI_SILU && (N % 128)) return ASTRAEA_EINVAL;
+  if (e->kind == EPI_QKV_ROPE) {
+    const astraea_kv_geometry& g = in->geo;
+    if (!in->pool_dev || !in->positions_dev || !in->slots_dev || (g.head_dim != 64 && g.head_dim != 128) ||
+        in->num_q_heads <= 0 || N != (in->num_q_heads + 2 * g.num_kv_heads) * g.head_dim || in->layer < 0 ||
+        in->layer >= g.num_layers)
+      return ASTRAEA_EINVAL;
+    e->pool = (bf16*)in->pool_dev;
+    e->block_el = (long long)g.num_layers * 2 * g.num_kv_heads * g.block_tokens * g.head_dim;
+    e->layer = in->layer;
+    e->Hq = in->num_q_heads;
+    e->Hkv = g.num_kv_heads;
+    e->D = g.head_dim;
+    e->bt = g.block_tokens;
+    e->pos = in->positions_dev;
+    e->slots = in->slots_dev;
+    e->theta = in->rope_theta;
+  }
   return 0;
 }
 
@@ -578,24 +797,25 @@ extern "C" size_t astraea_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K) 
   return sk_ws_bytes(M, sk_plan(M, N, K));
 }
 
-extern "C" int astraea_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, void* C, int32_t ldc,
-                                 int32_t M, int32_t N, int32_t K, const void* residual, int32_t epilogue,
-                                 void* ws, size_t ws_bytes, void* stream) {
-  if (M < 0 || N <= 0 || K <= 0 || lda < K || ldw < K || ldc < N) return ASTRAEA_EINVAL;
+extern "C" int astraea_gemm_bf16_ex(const void* A, int32_t lda, const void* W, int32_t ldw, void* C, int32_t ldc,
+                                    int32_t M, int32_t N, int32_t K, const astraea_epilogue* epi, void* ws,
+                                    size_t ws_bytes, void* stream) {
+  if (M < 0 || N <= 0 || K <= 0 || lda < K || ldw < K) return ASTRAEA_EINVAL;
   if ((lda % 8) || (ldw % 8) || (ldc % 8) || (N % 8)) return ASTRAEA_EINVAL;
-  if (epilogue == ASTRAEA_EPI_RESIDUAL && !residual) return ASTRAEA_EINVAL;
-  if (epilogue == ASTRAEA_EPI_NONE) residual = nullptr;
+  Epi e;
+  int rc = to_epi(epi, N, &e);
+  if (rc) return rc;
+  const int out_cols = e.kind == EPI_SILU ? N / 2 : (e.kind == EPI_QKV_ROPE ? e.Hq * e.D : N);
+  if (ldc < out_cols) return ASTRAEA_EINVAL;
   if (M == 0) return ASTRAEA_OK;
   cudaStream_t st = (cudaStream_t)stream;
   CUtensorMap ma, mb;
-  int rc;
   if (M <= kColsMaxM) {
     const SkPlan p = sk_plan(M, N, K);
     if (!ws || ws_bytes < sk_ws_bytes(M, p)) return ASTRAEA_EINVAL;
     if ((size_t)p.tiles * sizeof(int) > kCounterBytes) return ASTRAEA_EUNSUPPORTED;
     SkArgs a;
     a.C = (bf16*)C;
-    a.residual = (const bf16*)residual;
     a.counters = (int*)ws;
     a.ws = (float*)((char*)ws + kCounterBytes);
     a.M = M;
@@ -607,6 +827,7 @@ extern "C" int astraea_gemm_bf16(const void* A, int32_t lda, const void* W, int3
     a.grid = p.grid;
     a.maxseg = p.maxseg;
     a.units = p.units;
+    a.epi = e;
     if ((rc = make_map(&ma, W, N, K, ldw, kBM))) return rc;
     if ((rc = make_map(&mb, A, M, K, lda, p.bn))) return rc;
     if (p.bn == 16) return launch_sk<16>(ma, mb, a, st);
@@ -615,18 +836,25 @@ extern "C" int astraea_gemm_bf16(const void* A, int32_t lda, const void* W, int3
   }
   GemmArgs a;
   a.C = (bf16*)C;
-  a.residual = (const bf16*)residual;
-  a.ws = nullptr;
-  a.counters = nullptr;
   a.M = M;
   a.N = N;
   a.K = K;
   a.ldc = ldc;
-  a.kb_per_split = (K + kBK - 1) / kBK;
+  a.epi = e;
   const int bn = (N % 256 == 0 && (long long)((M + kBM - 1) / kBM) * (N / 256) >= num_sms()) ? 256 : 128;
   if ((rc = make_map(&ma, A, M, K, lda, kBM))) return rc;
   if ((rc = make_map(&mb, W, N, K, ldw, bn))) return rc;
   dim3 grid((M + kBM - 1) / kBM, (N + bn - 1) / bn, 1);
-  if (bn == 256) return launch<256, 4, kRows>(ma, mb, a, grid, st);
-  return launch<128, 6, kRows>(ma, mb, a, grid, st);
+  if (bn == 256) return launch_rows<256, 4>(ma, mb, a, grid, st);
+  return launch_rows<128, 6>(ma, mb, a, grid, st);
+}
+
+extern "C" int astraea_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, void* C, int32_t ldc,
+                                 int32_t M, int32_t N, int32_t K, const void* residual, int32_t epilogue,
+                                 void* ws, size_t ws_bytes, void* stream) {
+  if (epilogue != ASTRAEA_EPI_NONE && epilogue != ASTRAEA_EPI_RESIDUAL) return ASTRAEA_EINVAL;
+  astraea_epilogue e = {};
+  e.kind = epilogue;
+  e.residual_dev = residual;
+  return astraea_gemm_bf16_ex(A, lda, W, ldw, C, ldc, M, N, K, &e, ws, ws_bytes, stream);
 }

@@ -90,14 +90,31 @@ __global__ void silu_mul_kernel(const bf16* __restrict__ gu, bf16* __restrict__ 
 }
 
 __global__ void embedding_kernel(const int32_t* __restrict__ ids, const bf16* __restrict__ table,
-                                 bf16* __restrict__ out, int dim) {
+                                 bf16* __restrict__ out, int dim, float* __restrict__ ssq_out) {
   const long long t = blockIdx.x;
   pdl_wait();
   pdl_launch();
   const long long id = ids[t];
-  for (int i = threadIdx.x; i < dim / 8; i += blockDim.x)
-    *reinterpret_cast<uint4*>(out + t * dim + i * 8) =
-        *reinterpret_cast<const uint4*>(table + id * dim + i * 8);
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < dim / 8; i += blockDim.x) {
+    const uint4 u = *reinterpret_cast<const uint4*>(table + id * dim + i * 8);
+    *reinterpret_cast<uint4*>(out + t * dim + i * 8) = u;
+    float f[8];
+    unpack8(u, f);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ss += f[k] * f[k];
+  }
+  if (ssq_out) {
+    __shared__ float red[32];
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float s = 0.f;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+      ssq_out[t] = s;
+    }
+  }
 }
 
 __global__ void __launch_bounds__(1024) argmax_kernel(const bf16* __restrict__ logits, int vocab,
@@ -184,11 +201,11 @@ extern "C" int astraea_silu_mul(const void* gu, void* out, int32_t T, int32_t F,
 }
 
 extern "C" int astraea_embedding(const int32_t* ids, const void* table, void* out, int32_t T, int32_t dim,
-                                 void* stream) {
+                                 float* ssq_out, void* stream) {
   if (T < 0 || dim <= 0 || dim % 8) return ASTRAEA_EINVAL;
   if (T == 0) return ASTRAEA_OK;
   ASTRAEA_TRY(launch_k(embedding_kernel, dim3(T), dim3(128), 0, (cudaStream_t)stream, ids, (const bf16*)table,
-                       (bf16*)out, (int)dim));
+                       (bf16*)out, (int)dim, ssq_out));
   ASTRAEA_CHECK_LAUNCH();
   return ASTRAEA_OK;
 }

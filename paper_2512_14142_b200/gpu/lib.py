@@ -33,6 +33,30 @@ class KvGeometry(ctypes.Structure):
     ]
 
 
+class Epilogue(ctypes.Structure):
+    """astraea_epilogue (include/astraea_b200.h)."""
+
+    _fields_ = [
+        ("kind", ctypes.c_int32),
+        ("residual_dev", ctypes.c_void_p),
+        ("ssq_out_dev", ctypes.c_void_p),
+        ("ssq_in_dev", ctypes.c_void_p),
+        ("ssq_in_parts", ctypes.c_int32),
+        ("rms_dim", ctypes.c_int32),
+        ("rms_eps", ctypes.c_float),
+        ("pool_dev", ctypes.c_void_p),
+        ("geo", KvGeometry),
+        ("layer", ctypes.c_int32),
+        ("num_q_heads", ctypes.c_int32),
+        ("positions_dev", ctypes.c_void_p),
+        ("slots_dev", ctypes.c_void_p),
+        ("rope_theta", ctypes.c_float),
+    ]
+
+
+EPI_SILU = 2
+EPI_QKV_ROPE = 3
+
 _i32 = ctypes.c_int32
 _vp = ctypes.c_void_p
 _sz = ctypes.c_size_t
@@ -64,11 +88,13 @@ SIGNATURES = {
     "astraea_gemm_workspace_bytes": (_sz, [_i32, _i32, _i32]),
     "astraea_gemm_bf16": (
         ctypes.c_int, [_vp, _i32, _vp, _i32, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _sz, _vp]),
+    "astraea_gemm_bf16_ex": (
+        ctypes.c_int, [_vp, _i32, _vp, _i32, _vp, _i32, _i32, _i32, _i32, ctypes.POINTER(Epilogue), _vp, _sz, _vp]),
     "astraea_decode_advance": (
         ctypes.c_int, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp]),
     "astraea_rmsnorm": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _f32, _vp]),
     "astraea_silu_mul": (ctypes.c_int, [_vp, _vp, _i32, _i32, _vp]),
-    "astraea_embedding": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i32, _vp]),
+    "astraea_embedding": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i32, _vp, _vp]),
     "astraea_argmax": (ctypes.c_int, [_vp, _i32, _i32, _vp, _vp]),
 }
 

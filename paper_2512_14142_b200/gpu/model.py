@@ -6,15 +6,12 @@ those delays: the recompute-on-resume prefill and the paged decode step.
 Weights are random-init N(0, 0.02) with unit norms -- the
 data path's cost does not depend on the values.
 
-Per layer (bf16 activations, fp32 accumulation everywhere):
-  h   = rmsnorm(x)                                  K8
-  qkv = h @ Wqkv^T                                  K6/K9 tcgen05 GEMM
-  rope(q, k); append k, v to pool slots             K5
-  a   = paged attention (prefill K7 | decode K4)
-  x   = a @ Wo^T + x                                GEMM, residual fused in epilogue
-  h   = rmsnorm(x)
-  gu  = h @ Wgu^T ; m = silu(g) * u                 GEMM + K8
-  x   = m @ Wdown^T + x                             GEMM, residual fused
+Per layer (bf16 activations, fp32 accumulation everywhere), five launches:
+  q, k, v = rmsnorm(x) @ Wqkv^T ; rope ; k, v -> pool   one GEMM (K6/K9 + K5 fused)
+  a       = paged attention (prefill K7 | decode K4)
+  x       = a @ Wo^T + x                                 GEMM, residual + norm statistics fused
+  m       = silu(g) * u,  [g|u] = rmsnorm(x) @ Wgu^T     GEMM, RMS scale + SiLU fused (K8)
+  x       = m @ Wdown^T + x                              GEMM, residual + norm statistics fused
 then logits = rmsnorm(x_last) @ Wlm^T and greedy argmax.
 """
 
@@ -76,8 +73,28 @@ PRESETS = {
 }
 
 
+def interleave_gate_up(w_gu: torch.Tensor, ffn: int) -> torch.Tensor:
+    """[gate F | up F] rows -> [64 gate | 64 up] per 128 rows (SILU epilogue layout)."""
+    d = w_gu.shape[1]
+    g = w_gu[:ffn].view(ffn // 64, 64, d)
+    u = w_gu[ffn:].view(ffn // 64, 64, d)
+    return torch.stack([g, u], dim=1).reshape(2 * ffn, d)
+
+
+def deinterleave_gate_up(w: torch.Tensor, ffn: int) -> torch.Tensor:
+    d = w.shape[1]
+    v = w.view(ffn // 64, 2, 64, d)
+    return torch.cat([v[:, 0].reshape(ffn, d), v[:, 1].reshape(ffn, d)], dim=0)
+
+
 class LlamaWeights:
-    """Device-resident bf16 weights; deterministic for a (config, seed)."""
+    """Device-resident bf16 weights in the fused-epilogue layout.
+
+    Deterministic for a (config, seed). RMSNorm weights are folded into the
+    following projection (x*w @ W^T == x @ (W diag w)^T), and the gate/up
+    rows are interleaved per 64 for the SILU epilogue. ``to_cpu_dict``
+    returns the logical (textbook) weights for the oracle.
+    """
 
     def __init__(self, cfg: LlamaConfig, device="cuda", seed: int = 0, std: float = 0.02):
         self.cfg = cfg
@@ -89,32 +106,61 @@ class LlamaWeights:
             t.normal_(0.0, std, generator=g)
             return t
 
+        def fold(weight, norm):
+            return (weight.float() * norm.float()[None, :]).to(torch.bfloat16)
+
         d = cfg.hidden
+        ones = torch.ones(d, dtype=torch.bfloat16, device=device)
         self.embed = w(cfg.vocab, d)
         self.layers = []
         for _ in range(cfg.num_layers):
+            attn_norm, mlp_norm = ones.clone(), ones.clone()
+            wqkv = w(cfg.qkv_dim, d)
+            wo = w(d, cfg.num_q_heads * cfg.head_dim)
+            wgu = w(2 * cfg.ffn, d)
+            wdown = w(d, cfg.ffn)
             self.layers.append({
-                "attn_norm": torch.ones(d, dtype=torch.bfloat16, device=device),
-                "wqkv": w(cfg.qkv_dim, d),
-                "wo": w(d, cfg.num_q_heads * cfg.head_dim),
-                "mlp_norm": torch.ones(d, dtype=torch.bfloat16, device=device),
-                "wgu": w(2 * cfg.ffn, d),          # rows [0, F) gate, [F, 2F) up
-                "wdown": w(d, cfg.ffn),
+                "attn_norm": attn_norm,
+                "mlp_norm": mlp_norm,
+                "wqkv": fold(wqkv, attn_norm) if not bool((attn_norm == 1).all()) else wqkv,
+                "wo": wo,
+                "wgu": interleave_gate_up(fold(wgu, mlp_norm) if not bool((mlp_norm == 1).all()) else wgu, cfg.ffn),
+                "wdown": wdown,
             })
-        self.final_norm = torch.ones(d, dtype=torch.bfloat16, device=device)
+        self.final_norm = ones.clone()
         self.lm_head = w(cfg.vocab, d)
 
     def to_cpu_dict(self) -> dict:
-        return {
-            "embed": self.embed.cpu(),
-            "layers": [{k: v.cpu() for k, v in lw.items()} for lw in self.layers],
-            "final_norm": self.final_norm.cpu(),
-            "lm_head": self.lm_head.cpu(),
-        }
+        """Logical weights: un-interleaved gate/up, norms separate (the
+        stored projections are W diag(norm); with unit norms that is W)."""
+
+        def unfold(weight, norm):
+            return (weight.float() / norm.float()[None, :]).to(torch.bfloat16).cpu()
+
+        layers = []
+        for lw in self.layers:
+            layers.append({
+                "attn_norm": lw["attn_norm"].cpu(),
+                "mlp_norm": lw["mlp_norm"].cpu(),
+                "wqkv": unfold(lw["wqkv"], lw["attn_norm"]),
+                "wo": lw["wo"].cpu(),
+                "wgu": unfold(deinterleave_gate_up(lw["wgu"], self.cfg.ffn), lw["mlp_norm"]),
+                "wdown": lw["wdown"].cpu(),
+            })
+        return {"embed": self.embed.cpu(), "layers": layers, "final_norm": self.final_norm.cpu(),
+                "lm_head": unfold(self.lm_head, self.final_norm)}
 
 
 class LlamaRunner:
-    """Runs prefill / decode passes of one model against one KV pool."""
+    """Runs prefill / decode passes of one model against one KV pool.
+
+    Per layer, five launches: QKV GEMM (RMS scale + RoPE + KV append fused),
+    paged attention, O GEMM (+ residual, emits the next norm's statistics),
+    gate/up GEMM (RMS scale + SiLU*up fused), down GEMM (+ residual,
+    statistics). RMSNorm never runs as its own kernel: every GEMM that
+    consumes a normalised input scales its accumulator by rsqrt(mean x^2 +
+    eps) computed from per-128-column sums of squares its producer wrote.
+    """
 
     def __init__(self, weights: LlamaWeights, pool, max_tokens: int = 8192, max_rows: int = 64):
         self.w = weights
@@ -123,18 +169,18 @@ class LlamaRunner:
         dev = weights.embed.device
         cfg = self.cfg
         self.scale = 1.0 / math.sqrt(cfg.head_dim)
-        # split-K workspace for decode GEMMs (M <= 64): partials + arrival
-        # counters; zero-filled once, the kernel resets its counters.
         d = cfg.hidden
         shapes = [(cfg.qkv_dim, d), (d, cfg.num_q_heads * cfg.head_dim), (2 * cfg.ffn, d), (d, cfg.ffn),
                   (cfg.vocab, d)]
         lib = L.load()
         need = max(lib.astraea_gemm_workspace_bytes(64, n, k) for n, k in shapes)
+        # split-K workspace (partials + arrival counters): zero-filled once,
+        # the kernel resets its counters.
         self.gemm_ws = torch.zeros(need // 4 + 64, dtype=torch.float32, device=dev)
         self.max_rows = max_rows
         self.dec_ws = None
-        self.dec_ws_key = None
         self.device = dev
+        self.parts = -(-d // 128)
 
     def _dec_ws(self, B, max_blocks):
         need = L.load().astraea_decode_workspace_bytes(B, self.cfg.num_q_heads, self.cfg.head_dim, max_blocks)
@@ -143,28 +189,43 @@ class LlamaRunner:
                                                self.device)
         return self.dec_ws
 
-    def _layers(self, x, positions, slots, attend, stream=None):
+    def _embed(self, ids, stream):
+        T = ids.shape[0]
+        ssq = torch.empty(1, T, dtype=torch.float32, device=self.device)
+        x = ops.embedding(ids, self.w.embed, ssq_out=ssq, stream=stream)
+        return x, ssq
+
+    def _layers(self, x, ssq, positions, slots, attend, stream=None):
         cfg, w, pool = self.cfg, self.w, self.pool
         T = x.shape[0]
+        dev = x.device
         qd = cfg.num_q_heads * cfg.head_dim
+        q = torch.empty(T, qd, dtype=torch.bfloat16, device=dev)
+        att = torch.empty(T, qd, dtype=torch.bfloat16, device=dev)
+        h = torch.empty(T, cfg.ffn, dtype=torch.bfloat16, device=dev)
+        ssq_mid = torch.empty(self.parts, T, dtype=torch.float32, device=dev)
+        ssq_out = torch.empty(self.parts, T, dtype=torch.float32, device=dev)
+        ws = self.gemm_ws
+        d, eps = cfg.hidden, cfg.eps
         for li, lw in enumerate(w.layers):
-            h = ops.rmsnorm(x, lw["attn_norm"], cfg.eps, stream=stream)
-            qkv = ops.gemm(h, lw["wqkv"], workspace=self.gemm_ws, stream=stream)
-            ops.rope_kv_append(pool.geo, pool.data, li, qkv, cfg.num_q_heads, positions, slots,
-                               cfg.rope_theta, stream=stream)
-            att = torch.empty(T, qd, dtype=torch.bfloat16, device=x.device)
-            attend(li, qkv, att)
-            ops.gemm(att, lw["wo"], out=x, residual=x, workspace=self.gemm_ws, stream=stream)
-            h = ops.rmsnorm(x, lw["mlp_norm"], cfg.eps, stream=stream)
-            gu = ops.gemm(h, lw["wgu"], workspace=self.gemm_ws, stream=stream)
-            m = ops.silu_mul(gu, stream=stream)
-            ops.gemm(m, lw["wdown"], out=x, residual=x, workspace=self.gemm_ws, stream=stream)
-        return x
+            ops.gemm_ex(x, lw["wqkv"], q, kind=L.EPI_QKV_ROPE, ssq_in=ssq, rms_dim=d, rms_eps=eps, pool=pool.data,
+                        geo=pool.geo, layer=li, num_q_heads=cfg.num_q_heads, positions=positions, slots=slots,
+                        rope_theta=cfg.rope_theta, workspace=ws, stream=stream)
+            attend(li, q, att)
+            ops.gemm_ex(att, lw["wo"], x, kind=L.EPI_RESIDUAL, residual=x, ssq_out=ssq_mid, workspace=ws,
+                        stream=stream)
+            ops.gemm_ex(x, lw["wgu"], h, kind=L.EPI_SILU, ssq_in=ssq_mid, rms_dim=d, rms_eps=eps, workspace=ws,
+                        stream=stream)
+            ops.gemm_ex(h, lw["wdown"], x, kind=L.EPI_RESIDUAL, residual=x, ssq_out=ssq_out, workspace=ws,
+                        stream=stream)
+            ssq = ssq_out
+        return x, ssq
 
-    def _sample(self, x_rows, stream=None, want_logits=False, ids_out=None):
+    def _sample(self, x_rows, ssq_rows, stream=None, want_logits=False, ids_out=None):
         cfg = self.cfg
-        h = ops.rmsnorm(x_rows, self.w.final_norm, cfg.eps, stream=stream)
-        logits = ops.gemm(h, self.w.lm_head, workspace=self.gemm_ws, stream=stream)
+        logits = torch.empty(x_rows.shape[0], cfg.vocab, dtype=torch.bfloat16, device=x_rows.device)
+        ops.gemm_ex(x_rows, self.w.lm_head, logits, kind=L.EPI_NONE, ssq_in=ssq_rows, rms_dim=cfg.hidden,
+                    rms_eps=cfg.eps, workspace=self.gemm_ws, stream=stream)
         ids = ops.argmax(logits, out=ids_out, stream=stream)
         return (ids, logits) if want_logits else ids
 
@@ -173,25 +234,28 @@ class LlamaRunner:
         """Varlen prefill of S sequences; returns the greedy next token of each."""
         cfg = self.cfg
         S = ctx.shape[0]
-        x = ops.embedding(ids, self.w.embed, stream=stream)
+        x, ssq = self._embed(ids, stream)
+        qd = cfg.num_q_heads * cfg.head_dim
 
-        def attend(li, qkv, out):
-            ops.prefill_attention(self.pool.geo, self.pool.data, li, qkv, cfg.qkv_dim, cu_q, S, max_q_len,
+        def attend(li, q, out):
+            ops.prefill_attention(self.pool.geo, self.pool.data, li, q, qd, cu_q, S, max_q_len,
                                   cfg.num_q_heads, table, ctx, self.scale, out, stream=stream)
 
-        self._layers(x, positions, slots, attend, stream)
-        return self._sample(x.index_select(0, last_rows), stream, want_logits)
+        x, ssq = self._layers(x, ssq, positions, slots, attend, stream)
+        return self._sample(x.index_select(0, last_rows), ssq.index_select(1, last_rows).contiguous(), stream,
+                            want_logits)
 
     def decode(self, tokens, positions, slots, table, ctx, stream=None, want_logits=False, ids_out=None):
         """One decode step for B rows (retired rows: slot -1, ctx 0)."""
         cfg = self.cfg
         B = tokens.shape[0]
-        x = ops.embedding(tokens, self.w.embed, stream=stream)
+        x, ssq = self._embed(tokens, stream)
         ws = self._dec_ws(B, table.shape[1])
+        qd = cfg.num_q_heads * cfg.head_dim
 
-        def attend(li, qkv, out):
-            ops.decode_attention(self.pool.geo, self.pool.data, li, qkv, cfg.qkv_dim, B, cfg.num_q_heads,
+        def attend(li, q, out):
+            ops.decode_attention(self.pool.geo, self.pool.data, li, q, qd, B, cfg.num_q_heads,
                                  table, ctx, self.scale, out, ws, stream=stream)
 
-        self._layers(x, positions, slots, attend, stream)
-        return self._sample(x, stream, want_logits, ids_out)
+        x, ssq = self._layers(x, ssq, positions, slots, attend, stream)
+        return self._sample(x, ssq, stream, want_logits, ids_out)

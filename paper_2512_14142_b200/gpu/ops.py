@@ -61,6 +61,40 @@ def gemm(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None,
     return out
 
 
+def gemm_ex(a, w, out, kind=L.EPI_NONE, residual=None, ssq_out=None, ssq_in=None, rms_dim=0, rms_eps=1e-5,
+            pool=None, geo=None, layer=0, num_q_heads=0, positions=None, slots=None, rope_theta=0.0,
+            workspace=None, stream=None):
+    """GEMM with a fused epilogue program (astraea_gemm_bf16_ex)."""
+    lib = L.require_cuda()
+    M, K = a.shape
+    N = w.shape[0]
+    e = L.Epilogue()
+    e.kind = kind
+    e.residual_dev = L.ptr(residual)
+    e.ssq_out_dev = L.ptr(ssq_out)
+    e.ssq_in_dev = L.ptr(ssq_in)
+    e.ssq_in_parts = 0 if ssq_in is None else ssq_in.shape[0]
+    e.rms_dim = rms_dim
+    e.rms_eps = rms_eps
+    if kind == L.EPI_QKV_ROPE:
+        e.pool_dev = L.ptr(pool)
+        e.geo = geo
+        e.layer = layer
+        e.num_q_heads = num_q_heads
+        e.positions_dev = L.ptr(positions)
+        e.slots_dev = L.ptr(slots)
+        e.rope_theta = rope_theta
+    need = lib.astraea_gemm_workspace_bytes(M, N, K)
+    if need and (workspace is None or workspace.numel() * workspace.element_size() < need):
+        workspace = torch.zeros(need // 4 + 1, dtype=torch.float32, device=a.device)
+    L.check(lib.astraea_gemm_bf16_ex(
+        L.ptr(a), a.stride(0), L.ptr(w), w.stride(0), L.ptr(out), out.stride(0), M, N, K, ctypes.byref(e),
+        L.ptr(workspace), 0 if workspace is None else workspace.numel() * workspace.element_size(),
+        _s(stream)), "gemm_bf16_ex")
+    _count()
+    return out
+
+
 def rmsnorm(x, weight, eps, out=None, residual=None, resid_out=None, stream=None):
     lib = L.require_cuda()
     rows, dim = x.shape
@@ -83,13 +117,14 @@ def silu_mul(gu, out=None, stream=None):
     return out
 
 
-def embedding(ids, table, out=None, stream=None):
+def embedding(ids, table, out=None, ssq_out=None, stream=None):
     lib = L.require_cuda()
     T = ids.shape[0]
     dim = table.shape[1]
     if out is None:
         out = torch.empty(T, dim, dtype=table.dtype, device=table.device)
-    L.check(lib.astraea_embedding(L.ptr(ids), L.ptr(table), L.ptr(out), T, dim, _s(stream)), "embedding")
+    L.check(lib.astraea_embedding(L.ptr(ids), L.ptr(table), L.ptr(out), T, dim, L.ptr(ssq_out), _s(stream)),
+            "embedding")
     _count()
     return out
 

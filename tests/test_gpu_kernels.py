@@ -307,3 +307,78 @@ def test_decode_advance_drives_rows_and_records_history():
     assert seen[4][2] == [-1, -1, -1]
     h = hist.tolist()
     assert h[0][:3] == [7, 107, 207] and h[2][:2] == [9, 109] and h[1][:5] == [8, 108, 208, 308, 408]
+
+
+# ---------------------------------------------------------------- fused GEMM epilogues
+
+def _rms_parts(x, parts):
+    """Per-128-column sums of squares, [parts][M] (what a producer emits)."""
+    xf = x.float()
+    return torch.stack([xf[:, p * 128:(p + 1) * 128].pow(2).sum(-1) for p in range(parts)])
+
+
+@pytest.mark.parametrize("M", [3, 17, 64, 200])
+def test_gemm_residual_emits_norm_statistics(M):
+    N, K = 1024, 512
+    g = torch.Generator(device=DEV).manual_seed(M)
+    a = torch.randn(M, K, generator=g, device=DEV).bfloat16()
+    w = (torch.randn(N, K, generator=g, device=DEV) * 0.05).bfloat16()
+    x = torch.randn(M, N, generator=g, device=DEV).bfloat16()
+    ref = (a.float() @ w.float().T + x.float()).bfloat16()
+    ssq = torch.empty(N // 128, M, dtype=torch.float32, device=DEV)
+    ops.gemm_ex(a, w, x, kind=L.EPI_RESIDUAL, residual=x, ssq_out=ssq)
+    torch.cuda.synchronize()
+    assert rel_err(x, ref) < 5e-3
+    assert rel_err(ssq, _rms_parts(x, N // 128)) < 1e-5   # statistics of the stored bf16 output
+
+
+@pytest.mark.parametrize("M", [1, 16, 40, 150])
+def test_gemm_rms_scaled_silu(M):
+    F, K = 1536, 512
+    g = torch.Generator(device=DEV).manual_seed(7 + M)
+    x = torch.randn(M, K, generator=g, device=DEV).bfloat16()
+    wgu = (torch.randn(2 * F, K, generator=g, device=DEV) * 0.05).bfloat16()
+    from paper_2512_14142_b200.gpu.model import interleave_gate_up
+    ssq = _rms_parts(x, K // 128).contiguous()
+    out = torch.empty(M, F, dtype=torch.bfloat16, device=DEV)
+    ops.gemm_ex(x, interleave_gate_up(wgu, F).contiguous(), out, kind=L.EPI_SILU, ssq_in=ssq, rms_dim=K,
+                rms_eps=1e-5)
+    torch.cuda.synchronize()
+    h = x.float() * torch.rsqrt(x.float().pow(2).mean(-1, keepdim=True) + 1e-5)
+    gu = h @ wgu.float().T
+    ref = torch.nn.functional.silu(gu[:, :F]) * gu[:, F:]
+    assert rel_err(out, ref) < 1e-2
+
+
+@pytest.mark.parametrize("M", [2, 33, 130])
+@pytest.mark.parametrize("Hq,Hkv,D", [(32, 8, 128), (8, 2, 64)])
+def test_gemm_qkv_rope_append(M, Hq, Hkv, D):
+    K, Lyr, nb = 512, 2, 40
+    pool, geo = make_pool(nb, Lyr, Hkv, D)
+    pool.zero_()
+    g = torch.Generator(device=DEV).manual_seed(M + D)
+    x = torch.randn(M, K, generator=g, device=DEV).bfloat16()
+    w = (torch.randn((Hq + 2 * Hkv) * D, K, generator=g, device=DEV) * 0.05).bfloat16()
+    positions = torch.arange(50, 50 + M, dtype=torch.int32, device=DEV)
+    blocks = list(range(nb))[::-1]
+    slots = torch.tensor([blocks[p // 16] * 16 + p % 16 for p in range(50, 50 + M)], dtype=torch.int32,
+                         device=DEV)
+    slots[0] = -1
+    q = torch.empty(M, Hq * D, dtype=torch.bfloat16, device=DEV)
+    ssq = _rms_parts(x, K // 128).contiguous()
+    ops.gemm_ex(x, w, q, kind=L.EPI_QKV_ROPE, ssq_in=ssq, rms_dim=K, rms_eps=1e-5, pool=pool, geo=geo, layer=1,
+                num_q_heads=Hq, positions=positions, slots=slots, rope_theta=500000.0)
+    torch.cuda.synchronize()
+    h = x.float() * torch.rsqrt(x.float().pow(2).mean(-1, keepdim=True) + 1e-5)
+    qkv = (h @ w.float().T).bfloat16().float().cpu()
+    pc = positions.cpu()
+    q_ref = attention_ref.rope_ref(qkv[:, : Hq * D].view(M, Hq, D), pc, 500000.0)
+    k_ref = attention_ref.rope_ref(qkv[:, Hq * D:(Hq + Hkv) * D].view(M, Hkv, D), pc, 500000.0)
+    v_ref = qkv[:, (Hq + Hkv) * D:].view(M, Hkv, D)
+    assert rel_err(q.view(M, Hq, D), q_ref) < 1e-2
+    p6 = pool.view(nb, Lyr, 2, Hkv, 16, D).cpu().float()
+    ks = torch.stack([p6[int(s) // 16, 1, 0, :, int(s) % 16] for s in slots.tolist()[1:]])
+    vs = torch.stack([p6[int(s) // 16, 1, 1, :, int(s) % 16] for s in slots.tolist()[1:]])
+    assert rel_err(ks, k_ref[1:]) < 1e-2 and rel_err(vs, v_ref[1:]) < 1e-2
+    first = blocks[50 // 16] * 16 + 50 % 16
+    assert torch.count_nonzero(p6[first // 16, 1, :, :, first % 16]) == 0   # slot -1 skipped
