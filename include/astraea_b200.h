@@ -225,11 +225,17 @@ typedef struct {
   const int32_t* positions_dev;
   const int32_t* slots_dev;
   float rope_theta;
+  const float* rope_table_dev; /* optional [M][head_dim/2] (cos, sin) pairs from astraea_rope_table */
 } astraea_epilogue;
 ASTRAEA_API int astraea_gemm_bf16_ex(const void* A_dev, int32_t lda, const void* W_dev, int32_t ldw,
                          void* C_dev, int32_t ldc, int32_t M, int32_t N, int32_t K,
                          const astraea_epilogue* epilogue, void* workspace_dev,
                          size_t workspace_bytes, void* stream);
+
+/* RoPE angle table for a batch: table[t][i] = (cos, sin)(positions[t] * theta^(-2i/D)),
+ * i < D/2 -- computed once per forward and shared by every layer's QKV epilogue. */
+ASTRAEA_API int astraea_rope_table(const int32_t* positions_dev, int32_t T, int32_t head_dim, float rope_theta,
+                       float* table_dev, void* stream);
 
 /* ---- K8: small fused ops --------------------------------------------------------------------------- */
 /* y = rmsnorm(x + r) * w ; if resid_out_dev != NULL it receives x + r. r may be NULL. */

@@ -142,16 +142,21 @@ struct Epi {
   const int32_t* pos;
   const int32_t* slots;
   float theta;
+  const float2* cs;        // optional [M][D/2] (cos, sin) table
 };
+
+// (cos, sin) of token t's rotation for frequency index i (< D/2).
+__device__ __forceinline__ float2 rope_cs(const Epi& e, int t, int i) {
+  if (e.cs) return e.cs[(long long)t * (e.D / 2) + i];
+  float sn, cs;
+  sincosf((float)e.pos[t] * (1.0f / powf(e.theta, (float)(2 * i) / (float)e.D)), &sn, &cs);
+  return make_float2(cs, sn);
+}
 
 __device__ __forceinline__ float rms_scale(const Epi& e, int M, int t) {
   float s = 0.f;
   for (int p = 0; p < e.ssq_parts; ++p) s += e.ssq_in[(long long)p * M + t];
   return rsqrtf(s / (float)e.rms_dim + e.eps);
-}
-
-__device__ __forceinline__ float rope_inv_freq(const Epi& e, int i) {
-  return 1.0f / powf(e.theta, (float)(2 * i) / (float)e.D);
 }
 
 // Destination of a rotated/plain head element in QKV_ROPE: q -> C, k/v -> pool.
@@ -289,20 +294,39 @@ __global__ void __launch_bounds__(kThreads, 1)
               *reinterpret_cast<uint4*>(crow + f0 + j) = pack8(o);
             }
           } else {
-            const float pos = (float)e.pos[m];
+            // 32 consecutive columns of one head: low half hrow0.., high half +D/2
+            const int col0 = n_group + c * 32;
+            const int head = col0 / e.D, hrow0 = col0 % e.D;
+            const bool rot = head < e.Hq + e.Hkv;
+            float ylo[32], yhi[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              const int col = n_group + c * 32 + j;        // column of the low element
-              const int head = col / e.D, hrow = col % e.D;  // hrow < D/2
               const float x0 = round_bf(lo[j] * rs), x1 = round_bf(hi[j] * rs);
-              if (head < e.Hq + e.Hkv) {
-                float sn, cs;
-                sincosf(pos * rope_inv_freq(e, hrow), &sn, &cs);
-                qkv_store(e, args.C, args.ldc, m, head, hrow, x0 * cs - x1 * sn);
-                qkv_store(e, args.C, args.ldc, m, head, hrow + e.D / 2, x1 * cs + x0 * sn);
+              if (rot) {
+                const float2 r = rope_cs(e, m, hrow0 + j);
+                ylo[j] = x0 * r.x - x1 * r.y;
+                yhi[j] = x1 * r.x + x0 * r.y;
               } else {
-                qkv_store(e, args.C, args.ldc, m, head, hrow, x0);
-                qkv_store(e, args.C, args.ldc, m, head, hrow + e.D / 2, x1);
+                ylo[j] = x0;
+                yhi[j] = x1;
+              }
+            }
+            bf16* dst = nullptr;
+            long long half_stride = e.D / 2;
+            if (head < e.Hq) {
+              dst = args.C + (long long)m * args.ldc + head * e.D + hrow0;
+            } else if (e.slots[m] >= 0) {
+              const int slot = e.slots[m];
+              const int kv = head < e.Hq + e.Hkv ? 0 : 1;
+              const int hk = head - e.Hq - kv * e.Hkv;
+              dst = e.pool + (long long)(slot / e.bt) * e.block_el +
+                    ((long long)(e.layer * 2 + kv) * e.Hkv + hk) * e.bt * e.D + (long long)(slot % e.bt) * e.D + hrow0;
+            }
+            if (dst) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) {
+                *reinterpret_cast<uint4*>(dst + j) = pack8(ylo + j);
+                *reinterpret_cast<uint4*>(dst + half_stride + j) = pack8(yhi + j);
               }
             }
           }
@@ -444,8 +468,6 @@ __device__ __forceinline__ void sk_finish(const SkArgs& a, int tile, int row, fl
     const int head = f / e.D, hrow = f % e.D, half = e.D / 2;
     const int partner = row ^ half;
     const bool rot = head < e.Hq + e.Hkv;
-    float inv = 0.f;
-    if (rot) inv = rope_inv_freq(e, hrow % half);
     if (fok) {
 #pragma unroll 4
       for (int t = 0; t < BN; ++t) {
@@ -454,9 +476,8 @@ __device__ __forceinline__ void sk_finish(const SkArgs& a, int tile, int row, fl
         float y = x;
         if (rot) {
           const float xp = bf2f(xch[t * kBM + partner]);
-          float sn, cs;
-          sincosf((float)e.pos[t] * inv, &sn, &cs);
-          y = hrow < half ? x * cs - xp * sn : x * cs + xp * sn;
+          const float2 r = rope_cs(e, t, hrow % half);
+          y = hrow < half ? x * r.x - xp * r.y : x * r.x + xp * r.y;
         }
         qkv_store(e, a.C, a.ldc, t, head, hrow, y);
       }
@@ -625,6 +646,18 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
 }
 
+__global__ void rope_table_kernel(const int32_t* __restrict__ pos, int T, int half, float theta,
+                                  float2* __restrict__ out) {
+  pdl_wait();
+  pdl_launch();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < T * half; i += gridDim.x * blockDim.x) {
+    const int t = i / half, k = i % half;
+    float sn, cs;
+    sincosf((float)pos[t] * (1.0f / powf(theta, (float)(2 * k) / (float)(2 * half))), &sn, &cs);
+    out[i] = make_float2(cs, sn);
+  }
+}
+
 // ---- host side ----------------------------------------------------------------------------
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -786,11 +819,22 @@ int to_epi(const astraea_epilogue* in, int N, Epi* e) {
     e->pos = in->positions_dev;
     e->slots = in->slots_dev;
     e->theta = in->rope_theta;
+    e->cs = reinterpret_cast<const float2*>(in->rope_table_dev);
   }
   return 0;
 }
 
 }  // namespace
+
+extern "C" int astraea_rope_table(const int32_t* positions, int32_t T, int32_t head_dim, float theta,
+                                  float* table, void* stream) {
+  if (T < 0 || (head_dim != 64 && head_dim != 128) || !table) return ASTRAEA_EINVAL;
+  if (T == 0) return ASTRAEA_OK;
+  const int n = T * head_dim / 2;
+  ASTRAEA_TRY(launch_k(rope_table_kernel, dim3((n + 255) / 256), dim3(256), 0, (cudaStream_t)stream, positions,
+                       (int)T, (int)(head_dim / 2), theta, reinterpret_cast<float2*>(table)));
+  return ASTRAEA_OK;
+}
 
 extern "C" size_t astraea_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K) {
   if (M <= 0 || M > kColsMaxM || N <= 0 || K <= 0) return 0;

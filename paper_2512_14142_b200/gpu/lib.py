@@ -51,6 +51,7 @@ class Epilogue(ctypes.Structure):
         ("positions_dev", ctypes.c_void_p),
         ("slots_dev", ctypes.c_void_p),
         ("rope_theta", ctypes.c_float),
+        ("rope_table_dev", ctypes.c_void_p),
     ]
 
 
@@ -90,6 +91,7 @@ SIGNATURES = {
         ctypes.c_int, [_vp, _i32, _vp, _i32, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _sz, _vp]),
     "astraea_gemm_bf16_ex": (
         ctypes.c_int, [_vp, _i32, _vp, _i32, _vp, _i32, _i32, _i32, _i32, ctypes.POINTER(Epilogue), _vp, _sz, _vp]),
+    "astraea_rope_table": (ctypes.c_int, [_vp, _i32, _i32, _f32, _vp, _vp]),
     "astraea_decode_advance": (
         ctypes.c_int, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp]),
     "astraea_rmsnorm": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _f32, _vp]),

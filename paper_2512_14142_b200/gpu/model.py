@@ -207,10 +207,11 @@ class LlamaRunner:
         ssq_out = torch.empty(self.parts, T, dtype=torch.float32, device=dev)
         ws = self.gemm_ws
         d, eps = cfg.hidden, cfg.eps
+        cs = ops.rope_table(positions, cfg.head_dim, cfg.rope_theta, stream=stream)
         for li, lw in enumerate(w.layers):
             ops.gemm_ex(x, lw["wqkv"], q, kind=L.EPI_QKV_ROPE, ssq_in=ssq, rms_dim=d, rms_eps=eps, pool=pool.data,
                         geo=pool.geo, layer=li, num_q_heads=cfg.num_q_heads, positions=positions, slots=slots,
-                        rope_theta=cfg.rope_theta, workspace=ws, stream=stream)
+                        rope_theta=cfg.rope_theta, rope_table=cs, workspace=ws, stream=stream)
             attend(li, q, att)
             ops.gemm_ex(att, lw["wo"], x, kind=L.EPI_RESIDUAL, residual=x, ssq_out=ssq_mid, workspace=ws,
                         stream=stream)

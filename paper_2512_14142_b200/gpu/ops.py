@@ -63,7 +63,7 @@ def gemm(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None,
 
 def gemm_ex(a, w, out, kind=L.EPI_NONE, residual=None, ssq_out=None, ssq_in=None, rms_dim=0, rms_eps=1e-5,
             pool=None, geo=None, layer=0, num_q_heads=0, positions=None, slots=None, rope_theta=0.0,
-            workspace=None, stream=None):
+            rope_table=None, workspace=None, stream=None):
     """GEMM with a fused epilogue program (astraea_gemm_bf16_ex)."""
     lib = L.require_cuda()
     M, K = a.shape
@@ -84,6 +84,7 @@ def gemm_ex(a, w, out, kind=L.EPI_NONE, residual=None, ssq_out=None, ssq_in=None
         e.positions_dev = L.ptr(positions)
         e.slots_dev = L.ptr(slots)
         e.rope_theta = rope_theta
+        e.rope_table_dev = L.ptr(rope_table)
     need = lib.astraea_gemm_workspace_bytes(M, N, K)
     if need and (workspace is None or workspace.numel() * workspace.element_size() < need):
         workspace = torch.zeros(need // 4 + 1, dtype=torch.float32, device=a.device)
@@ -91,6 +92,16 @@ def gemm_ex(a, w, out, kind=L.EPI_NONE, residual=None, ssq_out=None, ssq_in=None
         L.ptr(a), a.stride(0), L.ptr(w), w.stride(0), L.ptr(out), out.stride(0), M, N, K, ctypes.byref(e),
         L.ptr(workspace), 0 if workspace is None else workspace.numel() * workspace.element_size(),
         _s(stream)), "gemm_bf16_ex")
+    _count()
+    return out
+
+
+def rope_table(positions, head_dim, theta, out=None, stream=None):
+    lib = L.require_cuda()
+    T = positions.shape[0]
+    if out is None:
+        out = torch.empty(T, head_dim // 2, 2, dtype=torch.float32, device=positions.device)
+    L.check(lib.astraea_rope_table(L.ptr(positions), T, head_dim, theta, L.ptr(out), _s(stream)), "rope_table")
     _count()
     return out
 
