@@ -17,6 +17,8 @@
 //   absolute positions.
 #include <math.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 using namespace astraea;
@@ -25,6 +27,7 @@ namespace {
 
 constexpr int kBT = 16;         // tokens per block
 constexpr int kStages = 4;      // decode smem ring depth
+constexpr int kMaxSplits = 64;  // context splits per (row, kv head)
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct DecodeParams {
@@ -196,22 +199,47 @@ __global__ void __launch_bounds__(128) decode_kernel(const __grid_constant__ Dec
     __syncthreads();
     if (s_last) {
       __threadfence();
+      // merge: per q head, log-sum-exp weights of all splits (split order)
+      __shared__ float wsh[G][kMaxSplits];
+      __shared__ float den_sh[G];
+      const long long bh0 = (long long)b * p.Hq + h * G;
+      for (int i = tid; i < G * p.splits; i += 128) {
+        const int g = i / p.splits, sp = i % p.splits;
+        wsh[g][sp] = __ldcg(p.ws_lse + (bh0 + g) * p.splits + sp);
+      }
+      __syncthreads();
+      if (tid < G) {
+        float mx = -INFINITY;
+        for (int sp = 0; sp < p.splits; ++sp) mx = fmaxf(mx, wsh[tid][sp]);
+        float den = 0.f;
+        for (int sp = 0; sp < p.splits; ++sp) {
+          const float w = (mx == -INFINITY || wsh[tid][sp] == -INFINITY) ? 0.f : exp2f(wsh[tid][sp] - mx);
+          wsh[tid][sp] = w;
+          den += w;
+        }
+        den_sh[tid] = den;
+      }
+      __syncthreads();
       const long long row0 = ((long long)b * p.Hq + hq) * p.splits;
-      float mx = -INFINITY;
-      for (int sp = 0; sp < p.splits; ++sp) mx = fmaxf(mx, __ldcg(p.ws_lse + row0 + sp));
-      float num[DPT], den = 0.f;
+      float num[DPT];
 #pragma unroll
       for (int i = 0; i < DPT; ++i) num[i] = 0.f;
-      if (mx != -INFINITY) {
-        for (int sp = 0; sp < p.splits; ++sp) {
-          const float ls = __ldcg(p.ws_lse + row0 + sp);
-          if (ls == -INFINITY) continue;
-          const float w = exp2f(ls - mx);
-          den += w;
+      int sp = 0;
+      for (; sp + 4 <= p.splits; sp += 4) {
+        float o[4][DPT];
 #pragma unroll
-          for (int i = 0; i < DPT; ++i) num[i] += w * __ldcg(p.ws_o + (row0 + sp) * D + pd + i);
-        }
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int i = 0; i < DPT; ++i) o[k][i] = __ldcg(p.ws_o + (row0 + sp + k) * D + pd + i);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int i = 0; i < DPT; ++i) num[i] += wsh[pg][sp + k] * o[k][i];
       }
+      for (; sp < p.splits; ++sp)
+#pragma unroll
+        for (int i = 0; i < DPT; ++i) num[i] += wsh[pg][sp] * __ldcg(p.ws_o + (row0 + sp) * D + pd + i);
+      const float den = den_sh[pg];
       bf16* out = p.out + ((long long)b * p.Hq + hq) * D + pd;
 #pragma unroll
       for (int i = 0; i < DPT; ++i) out[i] = f2bf(den > 0.f ? num[i] / den : 0.f);
@@ -444,14 +472,21 @@ __global__ void __launch_bounds__(128) prefill_kernel(const __grid_constant__ Pr
 }
 
 int decode_splits(int B, int Hkv, int max_blocks, int* bps) {
-  const int target = 4 * num_sms();
+  // Enough CTAs to cover the SMs, but at least kMinBlocks blocks (8 KiB of
+  // K+V per head per block) per CTA so per-CTA fixed costs stay small.
+  constexpr int kMinBlocks = 8;
+  const int target = 2 * num_sms();
   const int base = B * Hkv;
   int want = (target + base - 1) / base;
-  want = max(1, min(want, max_blocks));
+  want = max(1, min(want, (max_blocks + kMinBlocks - 1) / kMinBlocks));
   int per = (max_blocks + want - 1) / want;
-  per = max(per, 2);  // >= 32 tokens per split
+  int splits = (max_blocks + per - 1) / per;
+  if (splits > kMaxSplits) {
+    per = (max_blocks + kMaxSplits - 1) / kMaxSplits;
+    splits = (max_blocks + per - 1) / per;
+  }
   *bps = per;
-  return (max_blocks + per - 1) / per;
+  return splits;
 }
 
 }  // namespace
@@ -460,8 +495,8 @@ int decode_splits(int B, int Hkv, int max_blocks, int* bps) {
 constexpr size_t kDecCounterBytes = 4096 * sizeof(int);
 
 extern "C" size_t astraea_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t D, int32_t max_blocks) {
-  // Upper bound over any Hkv: splits <= max_blocks / 2 + 1.
-  const size_t splits = (size_t)max_blocks / 2 + 1;
+  // Upper bound over any B / Hkv (see decode_splits).
+  const size_t splits = (size_t)std::min(max_blocks, kMaxSplits);
   return kDecCounterBytes + (size_t)B * Hq * splits * (D + 1) * sizeof(float);
 }
 

@@ -154,8 +154,17 @@ __device__ __forceinline__ float2 rope_cs(const Epi& e, int t, int i) {
 }
 
 __device__ __forceinline__ float rms_scale(const Epi& e, int M, int t) {
+  // independent loads in groups of 8 (the sum order stays p = 0, 1, 2, ...)
   float s = 0.f;
-  for (int p = 0; p < e.ssq_parts; ++p) s += e.ssq_in[(long long)p * M + t];
+  int p = 0;
+  for (; p + 8 <= e.ssq_parts; p += 8) {
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldcg(e.ssq_in + (long long)(p + k) * M + t);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += v[k];
+  }
+  for (; p < e.ssq_parts; ++p) s += __ldcg(e.ssq_in + (long long)p * M + t);
   return rsqrtf(s / (float)e.rms_dim + e.eps);
 }
 
@@ -629,12 +638,16 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (s_last) {
         __threadfence();
         const float* base = args.ws + (tile * args.maxseg * (long long)args.M) * kBM + row;
+        // segment by segment: all BN loads of a segment are independent and in
+        // flight together; accumulation order is the segment order
 #pragma unroll
-        for (int t = 0; t < BN; ++t) {
-          float o = 0.f;
-          if (t < args.M)
-            for (int sg = 0; sg < nseg; ++sg) o += __ldcg(base + ((long long)sg * args.M + t) * kBM);
-          v[t] = o;
+        for (int t = 0; t < BN; ++t) v[t] = 0.f;
+        for (int sg = 0; sg < nseg; ++sg) {
+          float p[BN];
+#pragma unroll
+          for (int t = 0; t < BN; ++t) p[t] = t < args.M ? __ldcg(base + ((long long)sg * args.M + t) * kBM) : 0.f;
+#pragma unroll
+          for (int t = 0; t < BN; ++t) v[t] += p[t];
         }
         if (threadIdx.x == 64) args.counters[tile] = 0;
         sk_finish<BN>(args, (int)tile, row, v, rs, xch, red);

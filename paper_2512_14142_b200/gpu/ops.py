@@ -26,12 +26,6 @@ def _count(n=1):
     LAUNCHES[0] += n
 
 
-def decode_splits(B, Hkv, max_blocks, sms=148):
-    """Mirror of the library's split choice (attention.cu decode_splits)."""
-    target = 4 * sms
-    want = max(1, min(-(-target // (B * Hkv)), max_blocks))
-    per = max(-(-max_blocks // want), 2)
-    return -(-max_blocks // per)
 
 
 def geometry(num_layers, num_kv_heads, head_dim, num_blocks, block_tokens=16) -> L.KvGeometry:
