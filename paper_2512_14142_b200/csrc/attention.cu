@@ -45,153 +45,206 @@ struct DecodeParams {
   float scale_log2;
 };
 
+// Warp-per-tile decode attention. Each of the 4 warps owns a private 2-deep
+// ring of (K, V) page stages and processes tiles j = warp, warp + 4, ... of
+// the CTA's block range independently: scores with lanes split over
+// (token, head group), softmax with 16-lane shuffles, PV with lanes split
+// over head_dim. No block-wide barrier inside the tile loop; the 4 warp
+// states are merged once at the end.
 template <int D, int G>
 __global__ void __launch_bounds__(128) decode_kernel(const __grid_constant__ DecodeParams p) {
   constexpr int PAGE = kBT * D;             // elements per page
   constexpr int CPR = D / 8;                // 16-byte chunks per row
-  constexpr int CPT = CPR / 8;              // chunks per score thread (8 threads per token)
-  constexpr int TPH = 128 / G;              // PV threads per q head
-  constexpr int DPT = D / TPH;              // dims per PV thread
-  static_assert(DPT >= 1 && DPT <= 8, "PV mapping");
+  constexpr int WST = 2;                    // stages per warp
+  constexpr int HPL = G >= 2 ? G / 2 : 1;   // heads per lane in the score phase
+  constexpr int DPL = D / 32;               // dims per lane in the PV phase
 
-  __shared__ __align__(128) bf16 ks[kStages][PAGE];
-  __shared__ __align__(128) bf16 vs[kStages][PAGE];
-  __shared__ float qs[G][D];
-  __shared__ float sc[G][kBT];
-  __shared__ __align__(8) uint64_t bar[kStages];
+  extern __shared__ __align__(128) uint8_t dsm[];
+  bf16 (*ks)[PAGE] = reinterpret_cast<bf16 (*)[PAGE]>(dsm);                       // [4*WST][PAGE]
+  bf16 (*vs)[PAGE] = reinterpret_cast<bf16 (*)[PAGE]>(dsm + 4 * WST * PAGE * 2);  // [4*WST][PAGE]
+  float (*acc_w)[G][D] = reinterpret_cast<float (*)[G][D]>(dsm);                  // aliases ks after the loop
+  __shared__ __align__(16) float qs[G][D];
+  __shared__ __align__(8) uint64_t bar[4 * WST];
+  __shared__ float m_w[4][G], l_w[4][G];
 
   const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   pdl_wait();
   pdl_launch();
   const int ctx = p.ctx[b];
   const int nblk = (ctx + kBT - 1) / kBT;
   const int b0 = split * p.blocks_per_split;
   const int b1 = min(nblk, b0 + p.blocks_per_split);
-  const int ntile = b1 - b0;
+  const int ntile = max(0, b1 - b0);
 
   for (int i = tid; i < G * D; i += 128) {
     const int g = i / D, d = i % D;
-    qs[g][d] = bf2f(p.q[(long long)b * p.q_stride + (h * G + g) * D + d]);
+    qs[g][d] = bf2f(p.q[(long long)b * p.q_stride + (h * G + g) * D + d]) * p.scale_log2;
   }
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bar[s], 1);
-    fence_barrier_init();
-  }
+  if (tid < 4 * WST) mbar_init(&bar[tid], 1);
+  fence_barrier_init();
   __syncthreads();
 
   const int32_t* trow = p.table + (long long)b * p.max_blocks;
   const long long head_off = ((long long)p.layer * 2 * p.Hkv + h) * PAGE;
   const long long v_off = (long long)p.Hkv * PAGE;
-  auto issue = [&](int j) {
-    const int slot = j % kStages;
-    const long long base = (long long)trow[b0 + j] * p.block_el + head_off;
-    mbar_arrive_expect_tx(&bar[slot], 2 * PAGE * 2);
-    bulk_g2s(ks[slot], p.pool + base, PAGE * 2, &bar[slot]);
-    bulk_g2s(vs[slot], p.pool + base + v_off, PAGE * 2, &bar[slot]);
+  // tiles of this warp: j = warp + 4 k, k = 0, 1, ...
+  const int my_tiles = ntile > warp ? (ntile - warp + 3) / 4 : 0;
+  auto issue = [&](int k) {
+    const int st = warp * WST + (k % WST);
+    const long long base = (long long)trow[b0 + warp + 4 * k] * p.block_el + head_off;
+    mbar_arrive_expect_tx(&bar[st], 2 * PAGE * 2);
+    bulk_g2s(ks[st], p.pool + base, PAGE * 2, &bar[st]);
+    bulk_g2s(vs[st], p.pool + base + v_off, PAGE * 2, &bar[st]);
   };
-  if (tid == 0)
-    for (int j = 0; j < min(ntile, kStages); ++j) issue(j);
+  if (lane == 0)
+    for (int k = 0; k < min(my_tiles, WST); ++k) issue(k);
 
-  // score mapping
-  const int st = tid >> 3, part = tid & 7;
-  // PV mapping
-  const int pg = tid / TPH, pd = (tid % TPH) * DPT;
-  float m = -INFINITY, l = 0.f;
-  float acc[DPT];
+  const int t = lane & 15;          // score phase: token of this lane
+  const int hg = lane >> 4;         // head group (HPL heads)
+  float m[G], l[G], acc[G][DPL];
 #pragma unroll
-  for (int i = 0; i < DPT; ++i) acc[i] = 0.f;
-
-  for (int j = 0; j < ntile; ++j) {
-    const int slot = j % kStages;
-    const int valid = min(kBT, ctx - (b0 + j) * kBT);
-    mbar_wait(&bar[slot], (j / kStages) & 1);
-    // ---- scores: thread (token st, part) covers chunks part, part+8, ...
-    float dot[G];
+  for (int g = 0; g < G; ++g) {
+    m[g] = -INFINITY;
+    l[g] = 0.f;
 #pragma unroll
-    for (int g = 0; g < G; ++g) dot[g] = 0.f;
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-      const int chunk = part + 8 * c;
-      float kf[8];
-      unpack8(*reinterpret_cast<const uint4*>(&ks[slot][st * D + chunk * 8]), kf);
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const float4 q0 = *reinterpret_cast<const float4*>(&qs[g][chunk * 8]);
-        const float4 q1 = *reinterpret_cast<const float4*>(&qs[g][chunk * 8 + 4]);
-        dot[g] += q0.x * kf[0] + q0.y * kf[1] + q0.z * kf[2] + q0.w * kf[3] + q1.x * kf[4] +
-                  q1.y * kf[5] + q1.z * kf[6] + q1.w * kf[7];
-      }
-    }
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      dot[g] += __shfl_xor_sync(0xffffffffu, dot[g], 4);
-      dot[g] += __shfl_xor_sync(0xffffffffu, dot[g], 2);
-      dot[g] += __shfl_xor_sync(0xffffffffu, dot[g], 1);
-    }
-    if (part == 0) {
-#pragma unroll
-      for (int g = 0; g < G; ++g) sc[g][st] = st < valid ? dot[g] * p.scale_log2 : -INFINITY;
-    }
-    __syncthreads();
-    // ---- online softmax + PV for (head pg, dims pd..pd+DPT)
-    float mt = m;
-    for (int t = 0; t < valid; ++t) mt = fmaxf(mt, sc[pg][t]);
-    const float alpha = exp2f(m - mt);
-    l *= alpha;
-#pragma unroll
-    for (int i = 0; i < DPT; ++i) acc[i] *= alpha;
-    for (int t = 0; t < valid; ++t) {
-      const float pr = exp2f(sc[pg][t] - mt);
-      l += pr;
-      const bf16* vr = &vs[slot][t * D + pd];
-      if constexpr (DPT == 8) {
-        float vf[8];
-        unpack8(*reinterpret_cast<const uint4*>(vr), vf);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] += pr * vf[i];
-      } else if constexpr (DPT == 4) {
-        const uint2 u = *reinterpret_cast<const uint2*>(vr);
-        const float2 a0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-        const float2 a1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-        acc[0] += pr * a0.x; acc[1] += pr * a0.y; acc[2] += pr * a1.x; acc[3] += pr * a1.y;
-      } else if constexpr (DPT == 2) {
-        const float2 a0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr));
-        acc[0] += pr * a0.x; acc[1] += pr * a0.y;
-      } else {
-        acc[0] += pr * bf2f(*vr);
-      }
-    }
-    m = mt;
-    __syncthreads();  // slot and sc free
-    if (tid == 0 && j + kStages < ntile) issue(j + kStages);
+    for (int i = 0; i < DPL; ++i) acc[g][i] = 0.f;
   }
 
-  const int hq = h * G + pg;
-  if (p.splits == 1) {
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    float o[DPT];
+  for (int k = 0; k < my_tiles; ++k) {
+    const int j = warp + 4 * k;
+    const int st = warp * WST + (k % WST);
+    const int valid = min(kBT, ctx - (b0 + j) * kBT);
+    mbar_wait(&bar[st], (k / WST) & 1);
+    // ---- scores (log2 domain, q pre-scaled): lane -> token t, heads hg*HPL ..
+    float s[HPL];
 #pragma unroll
-    for (int i = 0; i < DPT; ++i) o[i] = acc[i] * inv;
-    bf16* dst = p.out + ((long long)b * p.Hq + hq) * D + pd;
-    if constexpr (DPT == 1) {
-      dst[0] = f2bf(o[0]);
-    } else {
+    for (int e = 0; e < HPL; ++e) s[e] = 0.f;
+    const bf16* krow = &ks[st][t * D];
+#pragma unroll 4
+    for (int c = 0; c < CPR; ++c) {
+      const int cc = (c + t) & (CPR - 1);   // rotate to spread smem banks across tokens
+      float kf[8];
+      unpack8(*reinterpret_cast<const uint4*>(krow + cc * 8), kf);
 #pragma unroll
-      for (int i = 0; i < DPT; i += 2)
-        *reinterpret_cast<__nv_bfloat162*>(dst + i) = __floats2bfloat162_rn(o[i], o[i + 1]);
+      for (int e = 0; e < HPL; ++e) {
+        const int g = hg * HPL + e;
+        if (g < G) {
+          const float4 q0 = *reinterpret_cast<const float4*>(&qs[g][cc * 8]);
+          const float4 q1 = *reinterpret_cast<const float4*>(&qs[g][cc * 8 + 4]);
+          s[e] += q0.x * kf[0] + q0.y * kf[1] + q0.z * kf[2] + q0.w * kf[3] + q1.x * kf[4] + q1.y * kf[5] +
+                  q1.z * kf[6] + q1.w * kf[7];
+        }
+      }
     }
+    // ---- online softmax per head over the 16 tokens of this tile. Lane
+    // half hg owns heads hg*HPL + e; m/l of all heads are replicated in
+    // every lane (register arrays, compile-time indexed only).
+    float pr[HPL], mnew[HPL], lnew[HPL], alpha[HPL];
+#pragma unroll
+    for (int e = 0; e < HPL; ++e) {
+      const int g = hg * HPL + e;
+      float mold = -INFINITY, lold = 0.f;
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg)
+        if (gg == g) {
+          mold = m[gg];
+          lold = l[gg];
+        }
+      const float sv = (t < valid && g < G) ? s[e] : -INFINITY;
+      float mx = sv;
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mnew[e] = fmaxf(mold, mx);
+      alpha[e] = mnew[e] == -INFINITY ? 1.f : exp2f(mold - mnew[e]);
+      pr[e] = sv == -INFINITY ? 0.f : exp2f(sv - mnew[e]);
+      float sum = pr[e];
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      lnew[e] = lold * alpha[e] + sum;
+    }
+    // broadcast per-head (m, alpha, l) to all lanes: head g lives in half g / HPL
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int src = (g / HPL) * 16;
+      const int e = g % HPL;
+      m[g] = __shfl_sync(0xffffffffu, mnew[e], src);
+      l[g] = __shfl_sync(0xffffffffu, lnew[e], src);
+      const float al = __shfl_sync(0xffffffffu, alpha[e], src);
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) acc[g][i] *= al;
+    }
+    // ---- PV: lane -> dims lane*DPL .. ; p[g][tok] from the score lanes
+    const bf16* vbase = &vs[st][lane * DPL];
+#pragma unroll 4
+    for (int tok = 0; tok < kBT; ++tok) {
+      if (tok >= valid) break;
+      float vf[DPL];
+      if constexpr (DPL == 4) {
+        const uint2 u = *reinterpret_cast<const uint2*>(vbase + tok * D);
+        const float2 a0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+        const float2 a1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+        vf[0] = a0.x; vf[1] = a0.y; vf[2] = a1.x; vf[3] = a1.y;
+      } else {
+        const float2 a0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vbase + tok * D));
+        vf[0] = a0.x; vf[1] = a0.y;
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float pg = __shfl_sync(0xffffffffu, pr[g % HPL], (g / HPL) * 16 + tok);
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) acc[g][i] += pg * vf[i];
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && k + WST < my_tiles) issue(k + WST);
+  }
+  // ---- merge the 4 warps (acc_w aliases the stage ring: wait for every warp)
+  __syncthreads();
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    if (lane == 0) {
+      m_w[warp][g] = m[g];
+      l_w[warp][g] = l[g];
+    }
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) acc_w[warp][g][lane * DPL + i] = acc[g][i];
+  }
+  __syncthreads();
+  constexpr int TPH = 128 / G;              // threads per head in the output phase
+  constexpr int DPT = D / TPH;
+  const int pg = tid / TPH, pd = (tid % TPH) * DPT;
+  float mt = -INFINITY;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) mt = fmaxf(mt, m_w[w][pg]);
+  float lsum = 0.f, o[DPT];
+#pragma unroll
+  for (int i = 0; i < DPT; ++i) o[i] = 0.f;
+  if (mt != -INFINITY) {
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float sc = m_w[w][pg] == -INFINITY ? 0.f : exp2f(m_w[w][pg] - mt);
+      lsum += l_w[w][pg] * sc;
+#pragma unroll
+      for (int i = 0; i < DPT; ++i) o[i] += acc_w[w][pg][pd + i] * sc;
+    }
+  }
+  const int hq = h * G + pg;
+  const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+  if (p.splits == 1) {
+    bf16* dst = p.out + ((long long)b * p.Hq + hq) * D + pd;
+#pragma unroll
+    for (int i = 0; i < DPT; ++i) dst[i] = f2bf(o[i] * inv);
   } else {
     // Split-K over the context: store this split's normalised partial and
     // log-sum-exp; the last split CTA of (row, kv head) to arrive merges all
     // splits in split order (deterministic) and writes the G output heads.
     __shared__ int s_last;
     const long long row = ((long long)b * p.Hq + hq) * p.splits + split;
-    const float inv = l > 0.f ? 1.f / l : 0.f;
     float* dst = p.ws_o + row * D + pd;
 #pragma unroll
-    for (int i = 0; i < DPT; ++i) __stcg(dst + i, acc[i] * inv);
-    if ((tid % TPH) == 0) __stcg(p.ws_lse + row, l > 0.f ? m + log2f(l) : -INFINITY);
+    for (int i = 0; i < DPT; ++i) __stcg(dst + i, o[i] * inv);
+    if ((tid % TPH) == 0) __stcg(p.ws_lse + row, lsum > 0.f ? mt + log2f(lsum) : -INFINITY);
     __threadfence();
     __syncthreads();
     int* ctr = p.counters + (long long)b * p.Hkv + h;
@@ -536,7 +589,17 @@ extern "C" int astraea_paged_decode_attention(const astraea_kv_geometry* g, cons
   p.ws_lse = p.ws_o + (size_t)B * Hq * p.splits * D;
   dim3 grid(p.splits, Hkv, B);
   cudaStream_t st = (cudaStream_t)stream;
-#define LAUNCH_DEC(DD, GG) ASTRAEA_TRY(launch_k(decode_kernel<DD, GG>, grid, dim3(128), 0, st, p))
+#define LAUNCH_DEC(DD, GG)                                                                         \
+  do {                                                                                               \
+    constexpr size_t smem = std::max<size_t>(2 * 8 * kBT * DD * 2, 4 * GG * DD * 4);                \
+    static bool attr = false;                                                                        \
+    if (!attr) {                                                                                     \
+      ASTRAEA_TRY(cudaFuncSetAttribute(decode_kernel<DD, GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                       (int)smem));                                                  \
+      attr = true;                                                                                   \
+    }                                                                                                \
+    ASTRAEA_TRY(launch_k(decode_kernel<DD, GG>, grid, dim3(128), smem, st, p));                     \
+  } while (0)
   if (D == 128 && G == 4) LAUNCH_DEC(128, 4);
   else if (D == 128 && G == 8) LAUNCH_DEC(128, 8);
   else if (D == 64 && G == 4) LAUNCH_DEC(64, 4);

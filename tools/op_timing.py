@@ -100,6 +100,21 @@ def main():
                                                        ssq_out=ssq2, workspace=ws))
     res["down_plain_gemm"] = timed(lambda: ops.gemm(h, lw["wdown"], workspace=ws))
     res["lm_head_gemm"] = timed(lambda: ops.gemm(x, w.lm_head, workspace=ws), reps=20)
+    def layer_seq():
+        ops.gemm_ex(x, lw["wqkv"], q, kind=L.EPI_QKV_ROPE, ssq_in=ssq, rms_dim=d, rms_eps=cfg.eps, pool=pool.data,
+                    geo=pool.geo, layer=0, num_q_heads=cfg.num_q_heads, positions=pos, slots=slots,
+                    rope_theta=cfg.rope_theta, rope_table=cs, workspace=ws)
+        ops.decode_attention(pool.geo, pool.data, 0, q, qd, B, cfg.num_q_heads, table, ctxd, r.scale, att, dws)
+        ops.gemm_ex(att, lw["wo"], x, kind=L.EPI_RESIDUAL, residual=x, ssq_out=ssq2, workspace=ws)
+        ops.gemm_ex(x, lw["wgu"], h, kind=L.EPI_SILU, ssq_in=ssq2, rms_dim=d, rms_eps=cfg.eps, workspace=ws)
+        ops.gemm_ex(h, lw["wdown"], x, kind=L.EPI_RESIDUAL, residual=x, ssq_out=ssq, workspace=ws)
+
+    res["layer_seq"] = timed(layer_seq, reps=32)
+    tokv = torch.zeros(B, dtype=torch.int32, device=dev)
+    res["embedding"] = timed(lambda: ops.embedding(tokv, w.embed, ssq_out=torch.empty(1, B, device=dev)))
+    res["rope_table"] = timed(lambda: ops.rope_table(pos, cfg.head_dim, cfg.rope_theta))
+    lg = torch.randn(B, cfg.vocab, device=dev).bfloat16()
+    res["argmax"] = timed(lambda: ops.argmax(lg))
     tok = torch.zeros(B, dtype=torch.int32, device=dev)
     out = torch.zeros(B, dtype=torch.int32, device=dev)
     res["decode_step"] = timed(lambda: r.decode(tok, pos, slots, table, ctxd, ids_out=out), reps=10)
