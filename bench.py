@@ -366,15 +366,15 @@ def decode_step_gbs(dp, cfg, B, ctx):
     pos = torch.full((B,), ctx, dtype=torch.int32, device="cuda")
     slots = table[:, ctx // 16] * 16 + ctx % 16
     ctxd = torch.full((B,), ctx + 1, dtype=torch.int32, device="cuda")
-    out = torch.zeros(B, dtype=torch.int32, device="cuda")
+    out = torch.zeros(B, dtype=torch.int64, device="cuda")
     for _ in range(3):
-        dp.runner.decode(tok, pos, slots, table, ctxd, ids_out=out)
+        dp.runner.decode(tok, pos, slots, table, ctxd, keys_out=out)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     n = 10
     e0.record()
     for _ in range(n):
-        dp.runner.decode(tok, pos, slots, table, ctxd, ids_out=out)
+        dp.runner.decode(tok, pos, slots, table, ctxd, keys_out=out)
     e1.record()
     e1.synchronize()
     ms = e0.elapsed_time(e1) / n

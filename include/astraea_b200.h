@@ -121,18 +121,19 @@ ASTRAEA_API int astraea_block_table_build(const int32_t* csr_ptr_dev, const int3
  * Advances the batch by one decode step without host involvement, so the
  * whole step (advance + layers + sampling) is one replayable graph.
  * step = *step_dev (then *step_dev += 1). For row b with step < n_gen[b]:
- *   fed token  = step == 0 ? first_tok[b] : sampled[b]
+ *   fed token  = step == 0 ? first_tok[b] : token of sampled_keys[b]
+ *                (an ARGMAX-epilogue key; the kernel re-zeroes it for the next step)
  *   position   = base_pos[b] + step;  ctx[b] = position + 1
  *   slot       = table[b][position / block_tokens] * block_tokens + position % block_tokens
  *   hist[b * hist_stride + step] = fed token
- * and at step == n_gen[b]: hist[b * hist_stride + n_gen[b]] = sampled[b] (the
+ * and at step == n_gen[b]: hist[b * hist_stride + n_gen[b]] = that token (the
  * row's pending next token), so hist rows need n_gen[b] + 1 entries.
  * Rows with step >= n_gen[b] are retired: slot -1, ctx 0 (attention and
  * append skip them) -- the compaction the reference's parallel-max batch
  * implies when members finish at their own n_gen (simulator.py:96-98). */
 ASTRAEA_API int astraea_decode_advance(int32_t* step_dev, int32_t B, const int32_t* n_gen_dev,
                            const int32_t* base_pos_dev, const int32_t* first_tok_dev,
-                           const int32_t* sampled_dev, const int32_t* table_dev,
+                           unsigned long long* sampled_keys_dev, const int32_t* table_dev,
                            int32_t max_blocks, int32_t block_tokens, int32_t* tokens_dev,
                            int32_t* positions_dev, int32_t* slots_dev, int32_t* ctx_dev,
                            int32_t* hist_dev, int32_t hist_stride, void* stream);
@@ -189,7 +190,8 @@ ASTRAEA_API int astraea_paged_prefill_attention(const astraea_kv_geometry* g, co
  * NULL when astraea_gemm_workspace_bytes() returns 0; otherwise it must be
  * zero-filled once before first use (its arrival counters are reset by the
  * kernel itself) and not shared by concurrently running GEMMs. */
-enum { ASTRAEA_EPI_NONE = 0, ASTRAEA_EPI_RESIDUAL = 1, ASTRAEA_EPI_SILU = 2, ASTRAEA_EPI_QKV_ROPE = 3 };
+enum { ASTRAEA_EPI_NONE = 0, ASTRAEA_EPI_RESIDUAL = 1, ASTRAEA_EPI_SILU = 2, ASTRAEA_EPI_QKV_ROPE = 3,
+       ASTRAEA_EPI_ARGMAX = 4 };
 ASTRAEA_API size_t astraea_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K);
 ASTRAEA_API int astraea_gemm_bf16(const void* A_dev, int32_t lda, const void* W_dev, int32_t ldw,
                       void* C_dev, int32_t ldc, int32_t M, int32_t N, int32_t K,
@@ -207,6 +209,10 @@ ASTRAEA_API int astraea_gemm_bf16(const void* A_dev, int32_t lda, const void* W_
  *   QKV_ROPE   N = (Hq + 2 Hkv) * head_dim: RoPE (theta, NeoX half split) on
  *              q and k at positions[t]; C[M][Hq*D] receives q; k and v rows
  *              are written to the pool at slots[t] (slot < 0: skipped)
+ *   ARGMAX     greedy sampling fused into the lm_head: atomicMax of a packed
+ *              (order-preserving value, ~column) key into argmax_keys[t]
+ *              (zero before the launch; lowest index wins ties); C may be
+ *              NULL, otherwise it also receives the bf16 logits
  * and for any program, input RMS scaling when ssq_in_dev != NULL:
  *   acc[t][:] *= rsqrt(sum_p ssq_in[p][t] / rms_dim + rms_eps)
  * (the norm weight is folded into W by the caller). */
@@ -226,6 +232,7 @@ typedef struct {
   const int32_t* slots_dev;
   float rope_theta;
   const float* rope_table_dev; /* optional [M][head_dim/2] (cos, sin) pairs from astraea_rope_table */
+  unsigned long long* argmax_keys_dev; /* ARGMAX: [M] */
 } astraea_epilogue;
 ASTRAEA_API int astraea_gemm_bf16_ex(const void* A_dev, int32_t lda, const void* W_dev, int32_t ldw,
                          void* C_dev, int32_t ldc, int32_t M, int32_t N, int32_t K,

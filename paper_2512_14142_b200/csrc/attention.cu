@@ -26,8 +26,8 @@ using namespace astraea;
 namespace {
 
 constexpr int kBT = 16;         // tokens per block
-constexpr int kStages = 4;      // decode smem ring depth
 constexpr int kMaxSplits = 64;  // context splits per (row, kv head)
+constexpr int kMaxBlocksPerSplit = 512;
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct DecodeParams {
@@ -77,22 +77,29 @@ __global__ void __launch_bounds__(128) decode_kernel(const __grid_constant__ Dec
   const int b1 = min(nblk, b0 + p.blocks_per_split);
   const int ntile = max(0, b1 - b0);
 
-  for (int i = tid; i < G * D; i += 128) {
-    const int g = i / D, d = i % D;
-    qs[g][d] = bf2f(p.q[(long long)b * p.q_stride + (h * G + g) * D + d]) * p.scale_log2;
+  // Block ids of this split (one per lane, loaded in parallel with q), so the
+  // first TMA issue does not wait on a dependent table load.
+  __shared__ int blk_ids[kMaxBlocksPerSplit];
+  const int32_t* trow = p.table + (long long)b * p.max_blocks;
+  for (int i = tid; i < ntile; i += 128) blk_ids[i] = trow[b0 + i];
+  for (int i = tid; i < G * D / 8; i += 128) {
+    const int g = i / (D / 8), c = i % (D / 8);
+    float f[8];
+    unpack8(*reinterpret_cast<const uint4*>(p.q + (long long)b * p.q_stride + (h * G + g) * D + c * 8), f);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) qs[g][c * 8 + k] = f[k] * p.scale_log2;
   }
   if (tid < 4 * WST) mbar_init(&bar[tid], 1);
   fence_barrier_init();
   __syncthreads();
 
-  const int32_t* trow = p.table + (long long)b * p.max_blocks;
   const long long head_off = ((long long)p.layer * 2 * p.Hkv + h) * PAGE;
   const long long v_off = (long long)p.Hkv * PAGE;
   // tiles of this warp: j = warp + 4 k, k = 0, 1, ...
   const int my_tiles = ntile > warp ? (ntile - warp + 3) / 4 : 0;
   auto issue = [&](int k) {
     const int st = warp * WST + (k % WST);
-    const long long base = (long long)trow[b0 + warp + 4 * k] * p.block_el + head_off;
+    const long long base = (long long)blk_ids[warp + 4 * k] * p.block_el + head_off;
     mbar_arrive_expect_tx(&bar[st], 2 * PAGE * 2);
     bulk_g2s(ks[st], p.pool + base, PAGE * 2, &bar[st]);
     bulk_g2s(vs[st], p.pool + base + v_off, PAGE * 2, &bar[st]);
@@ -538,6 +545,7 @@ int decode_splits(int B, int Hkv, int max_blocks, int* bps) {
     per = (max_blocks + kMaxSplits - 1) / kMaxSplits;
     splits = (max_blocks + per - 1) / per;
   }
+  if (per > kMaxBlocksPerSplit) return -1;   // > 64 x 512 x 16 tokens: not supported
   *bps = per;
   return splits;
 }
@@ -580,6 +588,7 @@ extern "C" int astraea_paged_decode_attention(const astraea_kv_geometry* g, cons
   p.scale_log2 = scale * kLog2e;
   int bps = 0;
   p.splits = decode_splits(B, Hkv, max_blocks, &bps);
+  if (p.splits < 0) return ASTRAEA_EUNSUPPORTED;
   p.blocks_per_split = bps;
   const size_t need = kDecCounterBytes + (size_t)B * Hq * p.splits * (D + 1) * sizeof(float);
   if (p.splits > 1 && (!ws || ws_bytes < need || (size_t)B * Hkv * sizeof(int) > kDecCounterBytes))

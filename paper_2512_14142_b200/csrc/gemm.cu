@@ -143,7 +143,27 @@ struct Epi {
   const int32_t* slots;
   float theta;
   const float2* cs;        // optional [M][D/2] (cos, sin) table
+  unsigned long long* amax;  // ARGMAX: [M] packed (value, index) keys
 };
+
+// Greedy-sampling key: order-preserving float bits in the high word, the
+// complemented column in the low word, so atomicMax picks the largest value
+// and, among equal values, the lowest index (torch.argmax's tie rule).
+__device__ __forceinline__ unsigned long long argmax_key(float x, int col) {
+  const uint32_t b = __float_as_uint(x);
+  const uint32_t u = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+  return ((unsigned long long)u << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)col);
+}
+
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
+  return a > b ? a : b;
+}
+
+__device__ __forceinline__ unsigned long long warp_max64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = umax64(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
 
 // (cos, sin) of token t's rotation for frequency index i (< D/2).
 __device__ __forceinline__ float2 rope_cs(const Epi& e, int t, int i) {
@@ -183,7 +203,7 @@ __device__ __forceinline__ void qkv_store(const Epi& e, bf16* C, int ldc, int t,
   base[(long long)off * e.D + hrow] = f2bf(y);
 }
 
-enum { EPI_NONE = 0, EPI_RESIDUAL = 1, EPI_SILU = 2, EPI_QKV_ROPE = 3 };
+enum { EPI_NONE = 0, EPI_RESIDUAL = 1, EPI_SILU = 2, EPI_QKV_ROPE = 3, EPI_ARGMAX = 4 };
 
 struct GemmArgs {
   bf16* C;
@@ -342,6 +362,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         continue;
       }
+      if (e.kind == EPI_ARGMAX) {
+        unsigned long long best = 0ull;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          float v[32];
+          tmem_ld32(lane_addr + g * 128 + c * 32, v);
+          const int n0 = n_group + c * 32;
+          if (!mok) continue;
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            if (n0 + k < args.N) {
+              const float o = v[k] * rs;
+              if (args.C) crow[n0 + k] = f2bf(o);
+              best = umax64(best, argmax_key(o, n0 + k));
+            }
+          }
+        }
+        if (mok) atomicMax(e.amax + m, best);
+        continue;
+      }
       float ssq = 0.f;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
@@ -431,6 +471,16 @@ __device__ __forceinline__ void sk_finish(const SkArgs& a, int tile, int row, fl
   if (e.ssq_in) {
 #pragma unroll
     for (int t = 0; t < BN; ++t) v[t] *= rs[t];
+  }
+  if (e.kind == EPI_ARGMAX) {
+#pragma unroll
+    for (int t = 0; t < BN; ++t) {
+      if (t >= M) break;
+      if (a.C && fok) a.C[(long long)t * a.ldc + f] = f2bf(v[t]);
+      const unsigned long long k = warp_max64(fok ? argmax_key(v[t], f) : 0ull);
+      if ((row & 31) == 0) atomicMax(e.amax + t, k);
+    }
+    return;
   }
   if (e.kind == EPI_NONE || e.kind == EPI_RESIDUAL) {
     float sq[BN];
@@ -805,7 +855,9 @@ int to_epi(const astraea_epilogue* in, int N, Epi* e) {
   *e = Epi{};
   if (!in) return 0;
   e->kind = in->kind;
-  if (in->kind < EPI_NONE || in->kind > EPI_QKV_ROPE) return ASTRAEA_EINVAL;
+  if (in->kind < EPI_NONE || in->kind > EPI_ARGMAX) return ASTRAEA_EINVAL;
+  e->amax = in->argmax_keys_dev;
+  if (e->kind == EPI_ARGMAX && !e->amax) return ASTRAEA_EINVAL;
   e->residual = (const bf16*)in->residual_dev;
   e->ssq_out = in->ssq_out_dev;
   e->ssq_in = in->ssq_in_dev;
@@ -863,7 +915,8 @@ extern "C" int astraea_gemm_bf16_ex(const void* A, int32_t lda, const void* W, i
   int rc = to_epi(epi, N, &e);
   if (rc) return rc;
   const int out_cols = e.kind == EPI_SILU ? N / 2 : (e.kind == EPI_QKV_ROPE ? e.Hq * e.D : N);
-  if (ldc < out_cols) return ASTRAEA_EINVAL;
+  if (C && ldc < out_cols) return ASTRAEA_EINVAL;
+  if (!C && e.kind != EPI_ARGMAX) return ASTRAEA_EINVAL;
   if (M == 0) return ASTRAEA_OK;
   cudaStream_t st = (cudaStream_t)stream;
   CUtensorMap ma, mb;

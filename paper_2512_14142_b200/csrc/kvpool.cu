@@ -362,9 +362,13 @@ extern "C" int astraea_rope_kv_append(const astraea_kv_geometry* g, void* pool, 
 // ---------------------------------------------------------------------------
 // Decode-loop driver: one CTA advances every row of the batch by one step.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ int key_token(unsigned long long k) {
+  return (int)(0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFull));
+}
+
 __global__ void decode_advance_kernel(int32_t* __restrict__ step_ctr, int B, const int32_t* __restrict__ n_gen,
                                       const int32_t* __restrict__ base_pos, const int32_t* __restrict__ first_tok,
-                                      const int32_t* __restrict__ sampled, const int32_t* __restrict__ table,
+                                      unsigned long long* __restrict__ keys, const int32_t* __restrict__ table,
                                       int max_blocks, int bt, int32_t* __restrict__ tokens,
                                       int32_t* __restrict__ positions, int32_t* __restrict__ slots,
                                       int32_t* __restrict__ ctx, int32_t* __restrict__ hist, int hist_stride) {
@@ -372,8 +376,10 @@ __global__ void decode_advance_kernel(int32_t* __restrict__ step_ctr, int B, con
   pdl_launch();
   const int step = *step_ctr;
   for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    const int sampled = step == 0 ? 0 : key_token(keys[b]);
+    keys[b] = 0ull;  // ready for this step's lm_head argmax
     if (step < n_gen[b]) {
-      const int tok = step == 0 ? first_tok[b] : sampled[b];
+      const int tok = step == 0 ? first_tok[b] : sampled;
       const int pos = base_pos[b] + step;
       tokens[b] = tok;
       positions[b] = pos;
@@ -383,7 +389,7 @@ __global__ void decode_advance_kernel(int32_t* __restrict__ step_ctr, int B, con
     } else {
       // first step after retirement: record the token sampled by the row's
       // last step (the request's pending next token)
-      if (hist && step == n_gen[b]) hist[(long long)b * hist_stride + step] = sampled[b];
+      if (hist && step == n_gen[b]) hist[(long long)b * hist_stride + step] = sampled;
       tokens[b] = 0;
       positions[b] = 0;
       ctx[b] = 0;
@@ -395,7 +401,7 @@ __global__ void decode_advance_kernel(int32_t* __restrict__ step_ctr, int B, con
 }
 
 extern "C" int astraea_decode_advance(int32_t* step, int32_t B, const int32_t* n_gen, const int32_t* base_pos,
-                                      const int32_t* first_tok, const int32_t* sampled, const int32_t* table,
+                                      const int32_t* first_tok, unsigned long long* sampled, const int32_t* table,
                                       int32_t max_blocks, int32_t bt, int32_t* tokens, int32_t* positions,
                                       int32_t* slots, int32_t* ctx, int32_t* hist, int32_t hist_stride,
                                       void* stream) {

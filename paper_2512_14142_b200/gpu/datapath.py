@@ -363,7 +363,7 @@ class KvDataPath:
             pos_d = torch.empty(B, dtype=torch.int32, device=dev)
             slot_d = torch.empty(B, dtype=torch.int32, device=dev)
             ctx_d = torch.empty(B, dtype=torch.int32, device=dev)
-            sampled = torch.zeros(B, dtype=torch.int32, device=dev)
+            sampled = torch.zeros(B, dtype=torch.int64, device=dev)   # argmax keys
             retire_at = set(n_gen)
             retire_ev = {}
             for s in range(max_ngen + 1):
@@ -371,7 +371,7 @@ class KvDataPath:
                                    tokens, pos_d, slot_d, ctx_d, hist, max_ngen + 1, stream=self.compute)
                 if s == max_ngen:
                     break
-                self.runner.decode(tokens, pos_d, slot_d, table, ctx_d, stream=self.compute, ids_out=sampled)
+                self.runner.decode(tokens, pos_d, slot_d, table, ctx_d, stream=self.compute, keys_out=sampled)
                 if (s + 1) in retire_at:
                     ev = torch.cuda.Event(enable_timing=True)
                     ev.record(self.compute)

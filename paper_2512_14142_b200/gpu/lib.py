@@ -52,11 +52,13 @@ class Epilogue(ctypes.Structure):
         ("slots_dev", ctypes.c_void_p),
         ("rope_theta", ctypes.c_float),
         ("rope_table_dev", ctypes.c_void_p),
+        ("argmax_keys_dev", ctypes.c_void_p),
     ]
 
 
 EPI_SILU = 2
 EPI_QKV_ROPE = 3
+EPI_ARGMAX = 4
 
 _i32 = ctypes.c_int32
 _vp = ctypes.c_void_p

@@ -222,12 +222,22 @@ class LlamaRunner:
             ssq = ssq_out
         return x, ssq
 
-    def _sample(self, x_rows, ssq_rows, stream=None, want_logits=False, ids_out=None):
+    def _sample(self, x_rows, ssq_rows, stream=None, want_logits=False, keys_out=None):
+        """Final norm + lm_head + greedy argmax in one GEMM (ARGMAX epilogue).
+
+        With ``keys_out`` (int64, zeroed) the packed argmax keys stay on the
+        device for ``decode_advance``; otherwise token ids are returned.
+        """
         cfg = self.cfg
-        logits = torch.empty(x_rows.shape[0], cfg.vocab, dtype=torch.bfloat16, device=x_rows.device)
-        ops.gemm_ex(x_rows, self.w.lm_head, logits, kind=L.EPI_NONE, ssq_in=ssq_rows, rms_dim=cfg.hidden,
-                    rms_eps=cfg.eps, workspace=self.gemm_ws, stream=stream)
-        ids = ops.argmax(logits, out=ids_out, stream=stream)
+        rows = x_rows.shape[0]
+        keys = keys_out if keys_out is not None else torch.zeros(rows, dtype=torch.int64, device=x_rows.device)
+        logits = (torch.empty(rows, cfg.vocab, dtype=torch.bfloat16, device=x_rows.device)
+                  if want_logits else None)
+        ops.gemm_ex(x_rows, self.w.lm_head, logits, kind=L.EPI_ARGMAX, ssq_in=ssq_rows, rms_dim=cfg.hidden,
+                    rms_eps=cfg.eps, argmax_keys=keys, workspace=self.gemm_ws, stream=stream)
+        if keys_out is not None:
+            return (keys_out, logits) if want_logits else keys_out
+        ids = ops.keys_to_ids(keys)
         return (ids, logits) if want_logits else ids
 
     def prefill(self, ids, positions, slots, cu_q, table, ctx, last_rows, max_q_len, stream=None,
@@ -246,8 +256,9 @@ class LlamaRunner:
         return self._sample(x.index_select(0, last_rows), ssq.index_select(1, last_rows).contiguous(), stream,
                             want_logits)
 
-    def decode(self, tokens, positions, slots, table, ctx, stream=None, want_logits=False, ids_out=None):
-        """One decode step for B rows (retired rows: slot -1, ctx 0)."""
+    def decode(self, tokens, positions, slots, table, ctx, stream=None, want_logits=False, keys_out=None):
+        """One decode step for B rows (retired rows: slot -1, ctx 0). With
+        ``keys_out`` the sampled tokens stay on the device as argmax keys."""
         cfg = self.cfg
         B = tokens.shape[0]
         x, ssq = self._embed(tokens, stream)
@@ -259,4 +270,4 @@ class LlamaRunner:
                                  table, ctx, self.scale, out, ws, stream=stream)
 
         x, ssq = self._layers(x, ssq, positions, slots, attend, stream)
-        return self._sample(x, ssq, stream, want_logits, ids_out)
+        return self._sample(x, ssq, stream, want_logits, keys_out)

@@ -57,7 +57,7 @@ def gemm(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None,
 
 def gemm_ex(a, w, out, kind=L.EPI_NONE, residual=None, ssq_out=None, ssq_in=None, rms_dim=0, rms_eps=1e-5,
             pool=None, geo=None, layer=0, num_q_heads=0, positions=None, slots=None, rope_theta=0.0,
-            rope_table=None, workspace=None, stream=None):
+            rope_table=None, argmax_keys=None, workspace=None, stream=None):
     """GEMM with a fused epilogue program (astraea_gemm_bf16_ex)."""
     lib = L.require_cuda()
     M, K = a.shape
@@ -70,6 +70,7 @@ def gemm_ex(a, w, out, kind=L.EPI_NONE, residual=None, ssq_out=None, ssq_in=None
     e.ssq_in_parts = 0 if ssq_in is None else ssq_in.shape[0]
     e.rms_dim = rms_dim
     e.rms_eps = rms_eps
+    e.argmax_keys_dev = L.ptr(argmax_keys)
     if kind == L.EPI_QKV_ROPE:
         e.pool_dev = L.ptr(pool)
         e.geo = geo
@@ -83,11 +84,17 @@ def gemm_ex(a, w, out, kind=L.EPI_NONE, residual=None, ssq_out=None, ssq_in=None
     if need and (workspace is None or workspace.numel() * workspace.element_size() < need):
         workspace = torch.zeros(need // 4 + 1, dtype=torch.float32, device=a.device)
     L.check(lib.astraea_gemm_bf16_ex(
-        L.ptr(a), a.stride(0), L.ptr(w), w.stride(0), L.ptr(out), out.stride(0), M, N, K, ctypes.byref(e),
+        L.ptr(a), a.stride(0), L.ptr(w), w.stride(0), L.ptr(out), out.stride(0) if out is not None else 0, M, N, K,
+        ctypes.byref(e),
         L.ptr(workspace), 0 if workspace is None else workspace.numel() * workspace.element_size(),
         _s(stream)), "gemm_bf16_ex")
     _count()
     return out
+
+
+def keys_to_ids(keys):
+    """Token ids from ARGMAX-epilogue keys (int64 view of the packed keys)."""
+    return (4294967295 - (keys & 4294967295)).to(torch.int32)
 
 
 def rope_table(positions, head_dim, theta, out=None, stream=None):

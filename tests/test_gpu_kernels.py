@@ -286,6 +286,11 @@ def test_rmsnorm_silu_embedding_argmax():
         [int(v) for v in logits.float().argmax(-1).tolist()[3:]]
 
 
+def _key(tok):
+    # ARGMAX-epilogue key of a token with some positive value (value bits irrelevant here)
+    return (0xC0000000 << 32) | (0xFFFFFFFF - tok)
+
+
 def test_decode_advance_drives_rows_and_records_history():
     B = 3
     dev = DEV
@@ -294,19 +299,41 @@ def test_decode_advance_drives_rows_and_records_history():
     first = torch.tensor([7, 8, 9], dtype=torch.int32, device=dev)
     table = torch.tensor([[5, 6, -1], [1, -1, -1], [2, 3, -1]], dtype=torch.int32, device=dev)
     step = torch.zeros(1, dtype=torch.int32, device=dev)
-    sampled = torch.zeros(B, dtype=torch.int32, device=dev)
+    keys = torch.zeros(B, dtype=torch.int64, device=dev)
     tok, pos, slot, ctx = (torch.empty(B, dtype=torch.int32, device=dev) for _ in range(4))
     hist = torch.zeros(B, 5, dtype=torch.int32, device=dev)
     seen = []
     for s in range(5):
-        ops.decode_advance(step, B, n_gen, base, first, sampled, table, 16, tok, pos, slot, ctx, hist, 5)
+        ops.decode_advance(step, B, n_gen, base, first, keys, table, 16, tok, pos, slot, ctx, hist, 5)
+        assert keys.tolist() == [0, 0, 0]            # advance re-zeroes the argmax keys
         seen.append((tok.tolist(), pos.tolist(), slot.tolist(), ctx.tolist()))
-        sampled.copy_(tok + 100)
+        keys.copy_(torch.tensor([_key(t + 100) for t in tok.tolist()], dtype=torch.int64))
     assert seen[0] == ([7, 8, 9], [10, 0, 31], [5 * 16 + 10, 16, 3 * 16 + 15], [11, 1, 32])
     assert seen[1] == ([107, 108, 0], [11, 1, 0], [5 * 16 + 11, 17, -1], [12, 2, 0])
     assert seen[4][2] == [-1, -1, -1]
     h = hist.tolist()
     assert h[0][:3] == [7, 107, 207] and h[2][:2] == [9, 109] and h[1][:5] == [8, 108, 208, 308, 408]
+
+
+@pytest.mark.parametrize("M", [1, 5, 64, 100])
+def test_gemm_argmax_epilogue_matches_torch(M):
+    V, K = 32000, 512
+    g = torch.Generator(device=DEV).manual_seed(M)
+    x = torch.randn(M, K, generator=g, device=DEV).bfloat16()
+    w = (torch.randn(V, K, generator=g, device=DEV) * 0.05).bfloat16()
+    ssq = _rms_parts(x, K // 128).contiguous()
+    keys = torch.zeros(M, dtype=torch.int64, device=DEV)
+    logits = torch.empty(M, V, dtype=torch.bfloat16, device=DEV)
+    ops.gemm_ex(x, w, logits, kind=L.EPI_ARGMAX, ssq_in=ssq, rms_dim=K, rms_eps=1e-5, argmax_keys=keys)
+    torch.cuda.synchronize()
+    h = x.float() * torch.rsqrt(x.float().pow(2).mean(-1, keepdim=True) + 1e-5)
+    ref = h @ w.float().T
+    ids = ops.keys_to_ids(keys).cpu()
+    top2 = ref.topk(2, dim=-1)
+    for r in range(M):
+        if float(top2.values[r, 0] - top2.values[r, 1]) > 1e-3:   # unambiguous winner
+            assert int(ids[r]) == int(top2.indices[r, 0])
+    assert rel_err(logits, ref) < 1e-2
 
 
 # ---------------------------------------------------------------- fused GEMM epilogues

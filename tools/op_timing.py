@@ -116,13 +116,13 @@ def main():
     lg = torch.randn(B, cfg.vocab, device=dev).bfloat16()
     res["argmax"] = timed(lambda: ops.argmax(lg))
     tok = torch.zeros(B, dtype=torch.int32, device=dev)
-    out = torch.zeros(B, dtype=torch.int32, device=dev)
-    res["decode_step"] = timed(lambda: r.decode(tok, pos, slots, table, ctxd, ids_out=out), reps=10)
+    out = torch.zeros(B, dtype=torch.int64, device=dev)
+    res["decode_step"] = timed(lambda: r.decode(tok, pos, slots, table, ctxd, keys_out=out), reps=10)
     import time
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(10):
-        r.decode(tok, pos, slots, table, ctxd, ids_out=out)
+        r.decode(tok, pos, slots, table, ctxd, keys_out=out)
     t_host = (time.perf_counter() - t0) / 10 * 1e6
     torch.cuda.synchronize()
     res["decode_step_host_issue"] = t_host

@@ -34,9 +34,9 @@ tok = torch.zeros(B, dtype=torch.int32, device="cuda")
 pos = torch.full((B,), ctx, dtype=torch.int32, device="cuda")
 slots = table[:, ctx // 16] * 16 + ctx % 16
 ctxd = torch.full((B,), ctx + 1, dtype=torch.int32, device="cuda")
-out = torch.zeros(B, dtype=torch.int32, device="cuda")
+out = torch.zeros(B, dtype=torch.int64, device="cuda")
 for _ in range(a.steps):
-    r.decode(tok, pos, slots, table, ctxd, ids_out=out)
+    r.decode(tok, pos, slots, table, ctxd, keys_out=out)
 if a.prefill:
     T = a.prefill
     blocks = list(range(B * nb, B * nb + (T + 15) // 16))
