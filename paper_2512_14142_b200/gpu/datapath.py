@@ -102,6 +102,9 @@ class KvDataPath:
                       "discards": 0, "recompute_tokens": 0, "h2d_bytes": 0, "d2h_bytes": 0,
                       "kernel_launches": 0}
         self.results: list = []     # (pinned hist copy, event, members) per batch for readback
+        self.use_graphs = True
+        self._graphs: dict = {}
+        self._graph_pool = None
         self.last_batch_events = None
         self.staged: dict = {}      # (request id, segment) -> device int32 prompt ids
 
@@ -356,26 +359,49 @@ class KvDataPath:
                     first_tok_parts.append(pend.view(1) if pend is not None
                                            else torch.zeros(1, dtype=torch.int32, device=dev))
             first_tok = torch.cat(first_tok_parts)
-            # ---- decode loop, driven on the device
-            step = torch.zeros(1, dtype=torch.int32, device=dev)
-            hist = torch.zeros(B, max_ngen + 1, dtype=torch.int32, device=dev)
-            tokens = torch.empty(B, dtype=torch.int32, device=dev)
-            pos_d = torch.empty(B, dtype=torch.int32, device=dev)
-            slot_d = torch.empty(B, dtype=torch.int32, device=dev)
-            ctx_d = torch.empty(B, dtype=torch.int32, device=dev)
-            sampled = torch.zeros(B, dtype=torch.int64, device=dev)   # argmax keys
+            # ---- decode loop, driven on the device (one CUDA-graph replay per step)
+            g = self._decode_graph(B, max_blocks) if (self.use_graphs and max_ngen <= self.HIST_MAX) else None
+            if g is not None:
+                gb = g["bufs"]
+                gb["step"].zero_()
+                gb["sampled"].zero_()
+                gb["n_gen"][:B].copy_(view("n_gen"))
+                gb["base_pos"][:B].copy_(view("base_pos"))
+                gb["first_tok"][:B].copy_(first_tok)
+                gb["table"].fill_(-1)
+                gb["table"][:, :max_blocks].copy_(table)
+                step, sampled, hist_buf = gb["step"], gb["sampled"], gb["hist"]
+                run_step = g["graph"].replay
+                adv_args = (gb["n_gen"], gb["base_pos"], gb["first_tok"], sampled, gb["table"], gb["tokens"],
+                            gb["pos"], gb["slots"], gb["ctx"], hist_buf, hist_buf.shape[1])
+            else:
+                step = torch.zeros(1, dtype=torch.int32, device=dev)
+                hist_buf = torch.zeros(B, max_ngen + 1, dtype=torch.int32, device=dev)
+                tokens = torch.empty(B, dtype=torch.int32, device=dev)
+                pos_d = torch.empty(B, dtype=torch.int32, device=dev)
+                slot_d = torch.empty(B, dtype=torch.int32, device=dev)
+                ctx_d = torch.empty(B, dtype=torch.int32, device=dev)
+                sampled = torch.zeros(B, dtype=torch.int64, device=dev)   # argmax keys
+                adv_args = (view("n_gen"), view("base_pos"), first_tok, sampled, table, tokens, pos_d, slot_d,
+                            ctx_d, hist_buf, max_ngen + 1)
+
+                def run_step():
+                    ops.decode_advance(step, B, adv_args[0], adv_args[1], adv_args[2], sampled, table, BT, tokens,
+                                       pos_d, slot_d, ctx_d, hist_buf, max_ngen + 1, stream=self.compute)
+                    self.runner.decode(tokens, pos_d, slot_d, table, ctx_d, stream=self.compute, keys_out=sampled)
             retire_at = set(n_gen)
             retire_ev = {}
-            for s in range(max_ngen + 1):
-                ops.decode_advance(step, B, view("n_gen"), view("base_pos"), first_tok, sampled, table, BT,
-                                   tokens, pos_d, slot_d, ctx_d, hist, max_ngen + 1, stream=self.compute)
-                if s == max_ngen:
-                    break
-                self.runner.decode(tokens, pos_d, slot_d, table, ctx_d, stream=self.compute, keys_out=sampled)
+            for s in range(max_ngen):
+                run_step()
                 if (s + 1) in retire_at:
                     ev = torch.cuda.Event(enable_timing=True)
                     ev.record(self.compute)
                     retire_ev[s + 1] = ev
+            # final advance: records every row's pending (next) token
+            n_gen_d, base_d, first_d, keys_d, table_d, tok_d, pos_dd, slot_dd, ctx_dd, hist_d, hstride = adv_args
+            ops.decode_advance(step, B, n_gen_d, base_d, first_d, keys_d, table_d, BT, tok_d, pos_dd, slot_dd,
+                               ctx_dd, hist_d, hstride, stream=self.compute)
+            hist = hist_buf[:B, : max_ngen + 1].clone()
             self.stats["decode_steps"] += max_ngen
             self.stats["decode_row_steps"] += sum(n_gen)
             # pending token recorded by the final advance
@@ -408,6 +434,47 @@ class KvDataPath:
             return None
         done_ev.synchronize()
         return [t_start.elapsed_time(retire_ev[p["n_gen"]]) / 1000.0 for p in plan]
+
+    HIST_MAX = 1024
+
+    def _decode_graph(self, B: int, max_blocks: int):
+        """One decode step (advance + full forward + fused sampling) captured
+        as a CUDA graph over persistent buffers, keyed by (B, block-table
+        width bucket). Replayed once per step; PDL edges are kept."""
+        mb = 1 << max(4, (max_blocks - 1).bit_length())   # power-of-two bucket >= 16
+        key = (B, mb)
+        g = self._graphs.get(key)
+        if g is not None:
+            return g
+        dev = self.device
+        i32 = dict(dtype=torch.int32, device=dev)
+        bufs = {
+            "step": torch.zeros(1, **i32), "n_gen": torch.zeros(B, **i32), "base_pos": torch.zeros(B, **i32),
+            "first_tok": torch.zeros(B, **i32), "sampled": torch.zeros(B, dtype=torch.int64, device=dev),
+            "table": torch.full((B, mb), -1, **i32), "tokens": torch.zeros(B, **i32), "pos": torch.zeros(B, **i32),
+            "slots": torch.full((B,), -1, **i32), "ctx": torch.zeros(B, **i32),
+            "hist": torch.zeros(B, self.HIST_MAX + 1, **i32),
+        }
+
+        def step():
+            ops.decode_advance(bufs["step"], B, bufs["n_gen"], bufs["base_pos"], bufs["first_tok"], bufs["sampled"],
+                               bufs["table"], BT, bufs["tokens"], bufs["pos"], bufs["slots"], bufs["ctx"],
+                               bufs["hist"], self.HIST_MAX + 1, stream=self.compute)
+            self.runner.decode(bufs["tokens"], bufs["pos"], bufs["slots"], bufs["table"], bufs["ctx"],
+                               stream=self.compute, keys_out=bufs["sampled"])
+
+        # warm-up (n_gen = 0: every row retired, nothing is written to the pool)
+        with torch.cuda.stream(self.compute):
+            step()
+        self.compute.synchronize()
+        if self._graph_pool is None:
+            self._graph_pool = torch.cuda.graph_pool_handle()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, pool=self._graph_pool, stream=self.compute):
+            step()
+        g = {"graph": graph, "bufs": bufs}
+        self._graphs[key] = g
+        return g
 
     # ------------------------------------------------------------------ end of run
 

@@ -179,12 +179,16 @@ class LlamaRunner:
         self.gemm_ws = torch.zeros(need // 4 + 64, dtype=torch.float32, device=dev)
         self.max_rows = max_rows
         self.dec_ws = None
+        self._old_ws = []
         self.device = dev
         self.parts = -(-d // 128)
 
     def _dec_ws(self, B, max_blocks):
         need = L.load().astraea_decode_workspace_bytes(B, self.cfg.num_q_heads, self.cfg.head_dim, max_blocks)
         if self.dec_ws is None or self.dec_ws.numel() * 4 < need:
+            # superseded buffers stay alive: captured CUDA graphs may still use them
+            if self.dec_ws is not None:
+                self._old_ws.append(self.dec_ws)
             self.dec_ws = ops.decode_workspace(B, self.cfg.num_q_heads, self.cfg.head_dim, max_blocks,
                                                self.device)
         return self.dec_ws

@@ -50,3 +50,16 @@ def test_measured_clock_produces_valid_report():
     host.audit_waste_log(rep)
     assert all(r.total_compute > 0 for r in rep.per_request)
     assert rep.requests_per_second() > 0
+
+
+def test_graph_and_eager_decode_paths_agree():
+    """CUDA-graph decode steps produce exactly the tokens of eager launches."""
+    name = "c1b200/6000"
+    toks = {}
+    for graphs in (True, False):
+        wl, pol, pred, mem, cfg = scenarios.build(host, name)
+        dp = datapath_for(mem.capacity_tokens)
+        dp.use_graphs = graphs
+        GpuEngine(wl, pol, pred, mem, cfg, dp).run()
+        toks[graphs] = [h.cpu().tolist() for _, h in dp.results]
+    assert toks[True] == toks[False]

@@ -288,7 +288,7 @@ def test_rmsnorm_silu_embedding_argmax():
 
 def _key(tok):
     # ARGMAX-epilogue key of a token with some positive value (value bits irrelevant here)
-    return (0xC0000000 << 32) | (0xFFFFFFFF - tok)
+    return (0x40000000 << 32) | (0xFFFFFFFF - tok)
 
 
 def test_decode_advance_drives_rows_and_records_history():
