@@ -444,6 +444,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // straddle warps (RoPE, gate/up) are exchanged through shared memory.
 // ---------------------------------------------------------------------------
 struct SkArgs {
+  unsigned long long* trace;   // diagnostics: [grid][8] globaltimer stamps, or NULL
   bf16* C;
   float* ws;        // [tiles][maxseg][M][128] partials
   int* counters;    // [tiles] arrival counters, zero between launches
@@ -452,6 +453,12 @@ struct SkArgs {
   long long units;
   Epi epi;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ int sk_owner(long long u, long long units, int grid) {
   return (int)(((u + 1) * grid - 1) / units);
@@ -568,6 +575,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
+  unsigned long long* tr = args.trace ? args.trace + (long long)cta * 8 : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = gtimer();
   const long long U = args.units;
   const long long u0 = (long long)cta * U / args.grid;
   const long long u1 = (long long)(cta + 1) * U / args.grid;
@@ -605,6 +614,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         tma_load_2d(sa + i * A_BYTES, &map_w, &full[i], (int)(u % KB) * kBK, (int)(u / KB) * kBM);
       }
       pdl_wait();
+      if (tr) tr[1] = gtimer();
       for (int i = 0; i < pre; ++i) tma_load_2d(sb + i * B_BYTES, &map_x, &full[i], (int)((u0 + i) % KB) * kBK, 0);
       int i = pre;
       for (long long u = u0 + pre; u < u1; ++u, ++i) {
@@ -633,6 +643,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         mbar_wait(&full[s], (i / STAGES) & 1);
         tc_fence_after();
         if (lane == 0) {
+          if (tr && i == 0) tr[2] = gtimer();
           const uint64_t da = smem_desc_sw128(sa + s * A_BYTES);
           const uint64_t db = smem_desc_sw128(sb + s * B_BYTES);
 #pragma unroll
@@ -642,6 +653,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         __syncwarp();
       }
+      if (tr && lane == 0 && u == u1) tr[3] = gtimer();
       if (lane == 0) mma_commit(&tfull[buf]);
       __syncwarp();
     }
@@ -703,10 +715,12 @@ __global__ void __launch_bounds__(kThreads, 2)
         sk_finish<BN>(args, (int)tile, row, v, rs, xch, red);
       }
     }
+    if (tr && threadIdx.x == 64) tr[4] = gtimer();
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
+  if (tr && threadIdx.x == 0) tr[5] = gtimer();
 }
 
 __global__ void rope_table_kernel(const int32_t* __restrict__ pos, int T, int half, float theta,
@@ -891,6 +905,17 @@ int to_epi(const astraea_epilogue* in, int N, Epi* e) {
 
 }  // namespace
 
+static unsigned long long* g_trace = nullptr;
+static int g_trace_slots = 0, g_trace_next = 0, g_trace_stride = 0;
+
+extern "C" int astraea_debug_gemm_trace(void* buf, int32_t slots, int32_t slot_stride) {
+  g_trace = (unsigned long long*)buf;
+  g_trace_slots = slots;
+  g_trace_stride = slot_stride;
+  g_trace_next = 0;
+  return ASTRAEA_OK;
+}
+
 extern "C" int astraea_rope_table(const int32_t* positions, int32_t T, int32_t head_dim, float theta,
                                   float* table, void* stream) {
   if (T < 0 || (head_dim != 64 && head_dim != 128) || !table) return ASTRAEA_EINVAL;
@@ -925,6 +950,11 @@ extern "C" int astraea_gemm_bf16_ex(const void* A, int32_t lda, const void* W, i
     if (!ws || ws_bytes < sk_ws_bytes(M, p)) return ASTRAEA_EINVAL;
     if ((size_t)p.tiles * sizeof(int) > kCounterBytes) return ASTRAEA_EUNSUPPORTED;
     SkArgs a;
+    a.trace = nullptr;
+    if (g_trace && g_trace_slots > 0) {
+      a.trace = g_trace + (size_t)(g_trace_next % g_trace_slots) * g_trace_stride;
+      ++g_trace_next;
+    }
     a.C = (bf16*)C;
     a.counters = (int*)ws;
     a.ws = (float*)((char*)ws + kCounterBytes);

@@ -73,6 +73,10 @@ def _blocks_for(tokens: int) -> int:
     return (tokens + BT - 1) // BT
 
 
+def _width_bucket(n: int) -> int:
+    return 1 << max(4, (n - 1).bit_length())
+
+
 def _loc(location) -> str:
     """Cache location by value, so states of the host mirror *and* of the
     unmodified reference package (its own CacheLocation enum) both work."""
@@ -281,7 +285,9 @@ class KvDataPath:
         for p in plan:
             csr_ids.extend(p["rd"].blocks)
             csr_ptr.append(len(csr_ids))
-        max_blocks = max(1, max(len(p["rd"].blocks) for p in plan))
+        # table width bucketed to a power of two (>= 16): the same kernel
+        # arguments whether the step runs eagerly or as a graph replay
+        max_blocks = _width_bucket(max(1, max(len(p["rd"].blocks) for p in plan)))
         positions, slots, cu_q, pre_ctx = [], [], [0], []
         for i in pre:
             p = plan[i]
@@ -371,7 +377,9 @@ class KvDataPath:
                 gb["table"].fill_(-1)
                 gb["table"][:, :max_blocks].copy_(table)
                 step, sampled, hist_buf = gb["step"], gb["sampled"], gb["hist"]
-                run_step = g["graph"].replay
+                def run_step(_g=g):
+                    _g["graph"].replay()
+                    ops.LAUNCHES[0] += _g["launches"]   # kernels inside the replayed graph
                 adv_args = (gb["n_gen"], gb["base_pos"], gb["first_tok"], sampled, gb["table"], gb["tokens"],
                             gb["pos"], gb["slots"], gb["ctx"], hist_buf, hist_buf.shape[1])
             else:
@@ -441,7 +449,7 @@ class KvDataPath:
         """One decode step (advance + full forward + fused sampling) captured
         as a CUDA graph over persistent buffers, keyed by (B, block-table
         width bucket). Replayed once per step; PDL edges are kept."""
-        mb = 1 << max(4, (max_blocks - 1).bit_length())   # power-of-two bucket >= 16
+        mb = _width_bucket(max_blocks)
         key = (B, mb)
         g = self._graphs.get(key)
         if g is not None:
@@ -470,9 +478,11 @@ class KvDataPath:
         if self._graph_pool is None:
             self._graph_pool = torch.cuda.graph_pool_handle()
         graph = torch.cuda.CUDAGraph()
+        n0 = ops.LAUNCHES[0]
         with torch.cuda.graph(graph, pool=self._graph_pool, stream=self.compute):
             step()
-        g = {"graph": graph, "bufs": bufs}
+        g = {"graph": graph, "bufs": bufs, "launches": ops.LAUNCHES[0] - n0}
+        ops.LAUNCHES[0] = n0
         self._graphs[key] = g
         return g
 

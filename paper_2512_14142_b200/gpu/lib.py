@@ -93,6 +93,7 @@ SIGNATURES = {
         ctypes.c_int, [_vp, _i32, _vp, _i32, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _sz, _vp]),
     "astraea_gemm_bf16_ex": (
         ctypes.c_int, [_vp, _i32, _vp, _i32, _vp, _i32, _i32, _i32, _i32, ctypes.POINTER(Epilogue), _vp, _sz, _vp]),
+    "astraea_debug_gemm_trace": (ctypes.c_int, [_vp, _i32, _i32]),
     "astraea_rope_table": (ctypes.c_int, [_vp, _i32, _i32, _f32, _vp, _vp]),
     "astraea_decode_advance": (
         ctypes.c_int, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp]),
