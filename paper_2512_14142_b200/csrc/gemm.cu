@@ -693,23 +693,52 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
       for (int t = 0; t < BN; ++t)
         if (t < args.M) __stcg(part + (long long)t * kBM + row, v[t]);
-      __threadfence();
+      // One release/acquire RMW per CTA after the barrier publishes the
+      // whole CTA's partial (cumulativity through bar.sync), instead of a
+      // fence in every thread.
       epi_bar();
-      if (threadIdx.x == 64) s_last = atomicAdd(args.counters + tile, 1) == nseg - 1;
+      if (threadIdx.x == 64) {
+        int prev;
+        asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(prev) : "l"(args.counters + tile) : "memory");
+        s_last = prev == nseg - 1;
+      }
       epi_bar();
       if (s_last) {
-        __threadfence();
         const float* base = args.ws + (tile * args.maxseg * (long long)args.M) * kBM + row;
-        // segment by segment: all BN loads of a segment are independent and in
-        // flight together; accumulation order is the segment order
+        // Partials are added in segment order (deterministic). For BN <= 32
+        // two segments' loads are in flight together and this CTA's own
+        // partial comes from registers; BN = 64 reloads it (register budget).
+        if constexpr (BN <= 32) {
+          float own[BN];
 #pragma unroll
-        for (int t = 0; t < BN; ++t) v[t] = 0.f;
-        for (int sg = 0; sg < nseg; ++sg) {
-          float p[BN];
+          for (int t = 0; t < BN; ++t) {
+            own[t] = v[t];
+            v[t] = 0.f;
+          }
+          for (int sg = 0; sg < nseg; sg += 2) {
+            float p0[BN], p1[BN];
 #pragma unroll
-          for (int t = 0; t < BN; ++t) p[t] = t < args.M ? __ldcg(base + ((long long)sg * args.M + t) * kBM) : 0.f;
+            for (int t = 0; t < BN; ++t) {
+              p0[t] = (t < args.M && sg != sidx) ? __ldcg(base + ((long long)sg * args.M + t) * kBM) : own[t];
+              p1[t] = (t < args.M && sg + 1 < nseg && sg + 1 != sidx)
+                          ? __ldcg(base + ((long long)(sg + 1) * args.M + t) * kBM) : own[t];
+            }
 #pragma unroll
-          for (int t = 0; t < BN; ++t) v[t] += p[t];
+            for (int t = 0; t < BN; ++t) {
+              v[t] += p0[t];
+              if (sg + 1 < nseg) v[t] += p1[t];
+            }
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < BN; ++t) v[t] = 0.f;
+          for (int sg = 0; sg < nseg; ++sg) {
+            float p0[BN];
+#pragma unroll
+            for (int t = 0; t < BN; ++t) p0[t] = t < args.M ? __ldcg(base + ((long long)sg * args.M + t) * kBM) : 0.f;
+#pragma unroll
+            for (int t = 0; t < BN; ++t) v[t] += p0[t];
+          }
         }
         if (threadIdx.x == 64) args.counters[tile] = 0;
         sk_finish<BN>(args, (int)tile, row, v, rs, xch, red);
