@@ -50,7 +50,9 @@ def parse():
     ap.add_argument("--model", default="llama3-8b")
     ap.add_argument("--requests", type=int, default=12, help="requests per rank")
     ap.add_argument("--qps", type=float, default=4.0, help="arrival rate per rank")
-    ap.add_argument("--capacity", type=int, default=6000, help="KV capacity (tokens) per GPU")
+    ap.add_argument("--capacity", type=int, default=3000,
+                    help="KV capacity (tokens) per GPU; 3000 puts the 12-request shard under memory pressure "
+                         "(preserve, swap and forced discard all occur)")
     ap.add_argument("--swap-mode", choices=("kernel", "dma"), default="kernel")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")

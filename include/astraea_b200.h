@@ -234,6 +234,27 @@ typedef struct {
   const float* rope_table_dev; /* optional [M][head_dim/2] (cos, sin) pairs from astraea_rope_table */
   unsigned long long* argmax_keys_dev; /* ARGMAX: [M] */
 } astraea_epilogue;
+/* A chain of dependent decode GEMMs (M <= 64 tokens) in ONE persistent launch
+ * (e.g. O-proj -> gate/up -> down -> next layer's QKV, or ... -> lm_head +
+ * argmax). Phase p+1 may read phase p's output: its activation tiles wait on
+ * a device-side phase barrier while its weight tiles already stream. At most
+ * 4 phases. workspace: astraea_gemm_chain_workspace_bytes(), zero-filled
+ * once before first use, not shared by concurrently running launches. */
+typedef struct {
+  const void* A;
+  int32_t lda;
+  const void* W;
+  int32_t ldw;
+  void* C;
+  int32_t ldc;
+  int32_t N;
+  int32_t K;
+  astraea_epilogue epi;
+} astraea_gemm_phase;
+ASTRAEA_API size_t astraea_gemm_chain_workspace_bytes(int32_t M, int32_t nphases,
+                                          const astraea_gemm_phase* phases);
+ASTRAEA_API int astraea_gemm_chain(int32_t M, int32_t nphases, const astraea_gemm_phase* phases,
+                       void* workspace_dev, size_t workspace_bytes, void* stream);
 ASTRAEA_API int astraea_gemm_bf16_ex(const void* A_dev, int32_t lda, const void* W_dev, int32_t ldw,
                          void* C_dev, int32_t ldc, int32_t M, int32_t N, int32_t K,
                          const astraea_epilogue* epilogue, void* workspace_dev,

@@ -443,15 +443,49 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Epilogue thread = one output feature of the tile, all M tokens; pairs that
 // straddle warps (RoPE, gate/up) are exchanged through shared memory.
 // ---------------------------------------------------------------------------
-struct SkArgs {
-  unsigned long long* trace;   // diagnostics: [grid][8] globaltimer stamps, or NULL
+// ---------------------------------------------------------------------------
+// Decode GEMM chain: persistent stream-K on tcgen05 (swap-AB orientation),
+// running up to kMaxPhases dependent GEMMs in one launch.
+//
+// Per phase, MMA A = W rows (128 output features per tile), MMA B = the M <= 64
+// tokens (BN = 16/32/64); the tiles x k-blocks units are split evenly over
+// one CTA per SM so every SM streams the same number of weight bytes (the
+// roofline of a decode step is the weight stream). A CTA walks its units in
+// order; the TMA ring runs continuously across tile *and phase* boundaries,
+// the MMA warp accumulates each tile segment into one of two TMEM
+// accumulators and the epilogue drains the other. Segments covering a whole
+// tile finish directly; split tiles are fixed up deterministically (each
+// segment stores an fp32 partial, the last to arrive sums them in segment
+// order and finishes).
+//
+// Phase p+1 reads phase p's output, so its activation tiles wait on a
+// device-side phase barrier (every CTA's epilogue arrives after finishing
+// phase p); its *weight* tiles do not, and stream into the ring while phase p
+// drains -- the same trick PDL plays at kernel boundaries (phase 0 waits on
+// griddepcontrol.wait instead).
+// ---------------------------------------------------------------------------
+constexpr int kMaxPhases = 4;
+
+struct SkPhase {
   bf16* C;
-  float* ws;        // [tiles][maxseg][M][128] partials
-  int* counters;    // [tiles] arrival counters, zero between launches
   int M, N, K, ldc;
-  int tiles, kbs, grid, maxseg;
+  int tiles, kbs, maxseg;
   long long units;
   Epi epi;
+};
+
+struct ChainMaps {
+  CUtensorMap w[kMaxPhases];
+  CUtensorMap x[kMaxPhases];
+};
+
+struct ChainArgs {
+  unsigned long long* trace;   // diagnostics: [grid][8] globaltimer stamps, or NULL
+  float* ws;                   // split-tile partials [tiles][maxseg][M][128] (reused by every phase)
+  int* counters;               // [tiles] arrival counters, zero between uses
+  int* phase_ctr;              // [kMaxPhases + 1] phase / kernel arrival counters, zero between launches
+  int M, grid, nph;
+  SkPhase ph[kMaxPhases];
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -466,10 +500,27 @@ __device__ __forceinline__ int sk_owner(long long u, long long units, int grid) 
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
+  int prev;
+  asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], %2;" : "=r"(prev) : "l"(p), "r"(v) : "memory");
+  return prev;
+}
+
+__device__ __forceinline__ void wait_phase(const int* ctr, int target) {
+  while (ld_acquire(ctr) < target) __nanosleep(32);
+}
+
+
 // Finish one 128-feature tile: thread `row` holds v[t] (t < M) of feature
 // tile*128 + row. All 128 epilogue threads call this together.
-template <int BN>
-__device__ __forceinline__ void sk_finish(const SkArgs& a, int tile, int row, float* v, const float* rs,
+template <int BN, typename A>
+__device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* v, const float* rs,
                                           bf16* xch, float* red) {
   const Epi& e = a.epi;
   const int M = a.M;
@@ -552,10 +603,9 @@ __device__ __forceinline__ void sk_finish(const SkArgs& a, int tile, int row, fl
   epi_bar();
 }
 
-template <int BN, int STAGES>
-__global__ void __launch_bounds__(kThreads, 2)
-    gemm_streamk_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
-                        const __grid_constant__ SkArgs args) {
+template <int BN, int STAGES, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+    gemm_chain_kernel(const __grid_constant__ ChainMaps maps, const __grid_constant__ ChainArgs args) {
   constexpr int A_BYTES = kBM * kBK * 2;
   constexpr int B_BYTES = BN * kBK * 2;
   constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
@@ -575,16 +625,15 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
+  const int G = args.grid;
   unsigned long long* tr = args.trace ? args.trace + (long long)cta * 8 : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = gtimer();
-  const long long U = args.units;
-  const long long u0 = (long long)cta * U / args.grid;
-  const long long u1 = (long long)(cta + 1) * U / args.grid;
-  const int KB = args.kbs;
 
   if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
+    for (int p = 0; p < args.nph; ++p) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.w[p]) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.x[p]) : "memory");
+    }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -604,152 +653,189 @@ __global__ void __launch_bounds__(kThreads, 2)
   pdl_launch();
   if (warp == 0) {
     if (lane == 0) {
-      // Weight tiles are independent of the previous kernel: stream the first
-      // STAGES of them while the predecessor drains, then wait for it and
-      // fetch the matching activation tiles.
-      const int pre = (int)(u1 - u0 < STAGES ? u1 - u0 : STAGES);
-      for (int i = 0; i < pre; ++i) {
-        const long long u = u0 + i;
-        mbar_arrive_expect_tx(&full[i], A_BYTES + B_BYTES);
-        tma_load_2d(sa + i * A_BYTES, &map_w, &full[i], (int)(u % KB) * kBK, (int)(u / KB) * kBM);
-      }
-      pdl_wait();
-      if (tr) tr[1] = gtimer();
-      for (int i = 0; i < pre; ++i) tma_load_2d(sb + i * B_BYTES, &map_x, &full[i], (int)((u0 + i) % KB) * kBK, 0);
-      int i = pre;
-      for (long long u = u0 + pre; u < u1; ++u, ++i) {
-        const int s = i % STAGES;
-        mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
-        mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
-        const int tile = (int)(u / KB), kc = (int)(u % KB) * kBK;
-        tma_load_2d(sa + s * A_BYTES, &map_w, &full[s], kc, tile * kBM);
-        tma_load_2d(sb + s * B_BYTES, &map_x, &full[s], kc, 0);
+      int i = 0;   // ring position, continuous across phases
+      for (int p = 0; p < args.nph; ++p) {
+        const SkPhase& P = args.ph[p];
+        const int KB = P.kbs;
+        const long long u0 = (long long)cta * P.units / G, u1 = (long long)(cta + 1) * P.units / G;
+        const int pre = (int)(u1 - u0 < STAGES ? u1 - u0 : STAGES);
+        // weights first: independent of the previous phase / kernel
+        for (int k = 0; k < pre; ++k) {
+          const int idx = i + k, s = idx % STAGES;
+          if (idx >= STAGES) mbar_wait(&empty[s], ((idx / STAGES) - 1) & 1);
+          const long long u = u0 + k;
+          mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
+          tma_load_2d(sa + s * A_BYTES, &maps.w[p], &full[s], (int)(u % KB) * kBK, (int)(u / KB) * kBM);
+        }
+        if (p == 0) {
+          pdl_wait();
+        } else {
+          wait_phase(args.phase_ctr + p - 1, G);
+          asm volatile("fence.proxy.async;" ::: "memory");   // generic-proxy writes -> TMA reads
+        }
+        if (tr && p == 0) tr[1] = gtimer();
+        for (int k = 0; k < pre; ++k) {
+          const int s = (i + k) % STAGES;
+          tma_load_2d(sb + s * B_BYTES, &maps.x[p], &full[s], (int)((u0 + k) % KB) * kBK, 0);
+        }
+        int idx = i + pre;
+        for (long long u = u0 + pre; u < u1; ++u, ++idx) {
+          const int s = idx % STAGES;
+          if (idx >= STAGES) mbar_wait(&empty[s], ((idx / STAGES) - 1) & 1);
+          mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
+          const int kc = (int)(u % KB) * kBK;
+          tma_load_2d(sa + s * A_BYTES, &maps.w[p], &full[s], kc, (int)(u / KB) * kBM);
+          tma_load_2d(sb + s * B_BYTES, &maps.x[p], &full[s], kc, 0);
+        }
+        i += (int)(u1 - u0);
       }
     }
   } else if (warp == 1) {
     pdl_wait();
     constexpr uint32_t idesc = instr_desc(BN);
     int i = 0, seg = 0;
-    for (long long u = u0; u < u1; ++seg) {
-      const long long tile = u / KB;
-      const long long seg_end = min(u1, (tile + 1) * KB);
-      const int buf = seg & 1;
-      if (seg >= 2) mbar_wait(&tempty[buf], ((seg >> 1) - 1) & 1);
-      tc_fence_after();
-      const uint32_t acc = tmem + buf * BN;
-      const long long seg_begin = u;
-      for (; u < seg_end; ++u, ++i) {
-        const int s = i % STAGES;
-        mbar_wait(&full[s], (i / STAGES) & 1);
+    for (int p = 0; p < args.nph; ++p) {
+      const SkPhase& P = args.ph[p];
+      const int KB = P.kbs;
+      const long long u0 = (long long)cta * P.units / G, u1 = (long long)(cta + 1) * P.units / G;
+      for (long long u = u0; u < u1; ++seg) {
+        const long long tile = u / KB;
+        const long long seg_end = min(u1, (tile + 1) * KB);
+        const int buf = seg & 1;
+        if (seg >= 2) mbar_wait(&tempty[buf], ((seg >> 1) - 1) & 1);
         tc_fence_after();
-        if (lane == 0) {
-          if (tr && i == 0) tr[2] = gtimer();
-          const uint64_t da = smem_desc_sw128(sa + s * A_BYTES);
-          const uint64_t db = smem_desc_sw128(sb + s * B_BYTES);
+        const uint32_t acc = tmem + buf * BN;
+        const long long seg_begin = u;
+        for (; u < seg_end; ++u, ++i) {
+          const int s = i % STAGES;
+          mbar_wait(&full[s], (i / STAGES) & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            if (tr && i == 0) tr[2] = gtimer();
+            const uint64_t da = smem_desc_sw128(sa + s * A_BYTES);
+            const uint64_t db = smem_desc_sw128(sb + s * B_BYTES);
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)
-            mma_bf16(acc, da + 2 * k, db + 2 * k, idesc, (u != seg_begin || k != 0) ? 1u : 0u);
-          mma_commit(&empty[s]);
+            for (int k = 0; k < kBK / 16; ++k)
+              mma_bf16(acc, da + 2 * k, db + 2 * k, idesc, (u != seg_begin || k != 0) ? 1u : 0u);
+            mma_commit(&empty[s]);
+          }
+          __syncwarp();
         }
+        if (lane == 0) mma_commit(&tfull[buf]);
         __syncwarp();
       }
-      if (tr && lane == 0 && u == u1) tr[3] = gtimer();
-      if (lane == 0) mma_commit(&tfull[buf]);
-      __syncwarp();
     }
+    if (tr && lane == 0) tr[3] = gtimer();
   } else {
     pdl_wait();
     const int quarter = warp & 3;
     const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
     const int row = quarter * 32 + lane;  // feature within the tile
-    if (args.epi.ssq_in) {
-      if (row < args.M) rs[row] = rms_scale(args.epi, args.M, row);
-      epi_bar();
-    }
     int seg = 0;
-    for (long long u = u0; u < u1; ++seg) {
-      const long long tile = u / KB;
-      const long long seg_end = min(u1, (tile + 1) * KB);
-      const bool whole = (u == tile * KB) && (seg_end == (tile + 1) * KB);
-      u = seg_end;
-      const int buf = seg & 1;
-      mbar_wait(&tfull[buf], (seg >> 1) & 1);
-      tc_fence_after();
-      float v[BN < 32 ? 32 : BN];
-#pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 32) tmem_ld32(lane_addr + buf * BN + c0, v + c0);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
-      if (whole) {
-        sk_finish<BN>(args, (int)tile, row, v, rs, xch, red);
-        continue;
+    for (int p = 0; p < args.nph; ++p) {
+      const SkPhase& P = args.ph[p];
+      const int KB = P.kbs;
+      const long long U = P.units;
+      const long long u0 = (long long)cta * U / G, u1 = (long long)(cta + 1) * U / G;
+      // Everything this phase's epilogue reads from earlier phases (residual,
+      // norm statistics) was published by those phases' barrier: acquire it
+      // once, then order the other epilogue threads behind it.
+      if (p > 0) {
+        if (threadIdx.x == 64) wait_phase(args.phase_ctr + p - 1, G);
+        epi_bar();
       }
-      const long long first_u = tile * KB;
-      const int c_first = sk_owner(first_u, U, args.grid);
-      const int nseg = sk_owner(first_u + KB - 1, U, args.grid) - c_first + 1;
-      const int sidx = cta - c_first;
-      float* part = args.ws + ((tile * args.maxseg + sidx) * (long long)args.M) * kBM;
-#pragma unroll
-      for (int t = 0; t < BN; ++t)
-        if (t < args.M) __stcg(part + (long long)t * kBM + row, v[t]);
-      // One release/acquire RMW per CTA after the barrier publishes the
-      // whole CTA's partial (cumulativity through bar.sync), instead of a
-      // fence in every thread.
-      epi_bar();
-      if (threadIdx.x == 64) {
-        int prev;
-        asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(prev) : "l"(args.counters + tile) : "memory");
-        s_last = prev == nseg - 1;
+      if (P.epi.ssq_in) {
+        if (row < args.M) rs[row] = rms_scale(P.epi, args.M, row);
+        epi_bar();
       }
-      epi_bar();
-      if (s_last) {
-        const float* base = args.ws + (tile * args.maxseg * (long long)args.M) * kBM + row;
-        // Partials are added in segment order (deterministic). For BN <= 32
-        // two segments' loads are in flight together and this CTA's own
-        // partial comes from registers; BN = 64 reloads it (register budget).
-        if constexpr (BN <= 32) {
-          float own[BN];
+      for (long long u = u0; u < u1; ++seg) {
+        const long long tile = u / KB;
+        const long long seg_end = min(u1, (tile + 1) * KB);
+        const bool whole = (u == tile * KB) && (seg_end == (tile + 1) * KB);
+        u = seg_end;
+        const int buf = seg & 1;
+        mbar_wait(&tfull[buf], (seg >> 1) & 1);
+        tc_fence_after();
+        float v[BN < 32 ? 32 : BN];
 #pragma unroll
-          for (int t = 0; t < BN; ++t) {
-            own[t] = v[t];
-            v[t] = 0.f;
-          }
-          for (int sg = 0; sg < nseg; sg += 2) {
-            float p0[BN], p1[BN];
-#pragma unroll
-            for (int t = 0; t < BN; ++t) {
-              p0[t] = (t < args.M && sg != sidx) ? __ldcg(base + ((long long)sg * args.M + t) * kBM) : own[t];
-              p1[t] = (t < args.M && sg + 1 < nseg && sg + 1 != sidx)
-                          ? __ldcg(base + ((long long)(sg + 1) * args.M + t) * kBM) : own[t];
-            }
-#pragma unroll
-            for (int t = 0; t < BN; ++t) {
-              v[t] += p0[t];
-              if (sg + 1 < nseg) v[t] += p1[t];
-            }
-          }
-        } else {
-#pragma unroll
-          for (int t = 0; t < BN; ++t) v[t] = 0.f;
-          for (int sg = 0; sg < nseg; ++sg) {
-            float p0[BN];
-#pragma unroll
-            for (int t = 0; t < BN; ++t) p0[t] = t < args.M ? __ldcg(base + ((long long)sg * args.M + t) * kBM) : 0.f;
-#pragma unroll
-            for (int t = 0; t < BN; ++t) v[t] += p0[t];
-          }
+        for (int c0 = 0; c0 < BN; c0 += 32) tmem_ld32(lane_addr + buf * BN + c0, v + c0);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+        if (whole) {
+          sk_finish<BN>(P, (int)tile, row, v, rs, xch, red);
+          continue;
         }
-        if (threadIdx.x == 64) args.counters[tile] = 0;
-        sk_finish<BN>(args, (int)tile, row, v, rs, xch, red);
+        const long long first_u = tile * KB;
+        const int c_first = sk_owner(first_u, U, G);
+        const int nseg = sk_owner(first_u + KB - 1, U, G) - c_first + 1;
+        const int sidx = cta - c_first;
+        float* part = args.ws + ((tile * P.maxseg + sidx) * (long long)args.M) * kBM;
+#pragma unroll
+        for (int t = 0; t < BN; ++t)
+          if (t < args.M) __stcg(part + (long long)t * kBM + row, v[t]);
+        // One release/acquire RMW per CTA after the barrier publishes the
+        // whole CTA's partial (cumulativity through bar.sync).
+        epi_bar();
+        if (threadIdx.x == 64) s_last = atom_add_acq_rel(args.counters + tile, 1) == nseg - 1;
+        epi_bar();
+        if (s_last) {
+          const float* base = args.ws + (tile * P.maxseg * (long long)args.M) * kBM + row;
+          // Partials are added in segment order (deterministic). For BN <= 32
+          // two segments' loads are in flight together and this CTA's own
+          // partial comes from registers; BN = 64 reloads it (register budget).
+          if constexpr (BN <= 32) {
+            float own[BN];
+#pragma unroll
+            for (int t = 0; t < BN; ++t) {
+              own[t] = v[t];
+              v[t] = 0.f;
+            }
+            for (int sg = 0; sg < nseg; sg += 2) {
+              float p0[BN], p1[BN];
+#pragma unroll
+              for (int t = 0; t < BN; ++t) {
+                p0[t] = (t < args.M && sg != sidx) ? __ldcg(base + ((long long)sg * args.M + t) * kBM) : own[t];
+                p1[t] = (t < args.M && sg + 1 < nseg && sg + 1 != sidx)
+                            ? __ldcg(base + ((long long)(sg + 1) * args.M + t) * kBM) : own[t];
+              }
+#pragma unroll
+              for (int t = 0; t < BN; ++t) {
+                v[t] += p0[t];
+                if (sg + 1 < nseg) v[t] += p1[t];
+              }
+            }
+          } else {
+#pragma unroll
+            for (int t = 0; t < BN; ++t) v[t] = 0.f;
+            for (int sg = 0; sg < nseg; ++sg) {
+              float p0[BN];
+#pragma unroll
+              for (int t = 0; t < BN; ++t) p0[t] = t < args.M ? __ldcg(base + ((long long)sg * args.M + t) * kBM) : 0.f;
+#pragma unroll
+              for (int t = 0; t < BN; ++t) v[t] += p0[t];
+            }
+          }
+          if (threadIdx.x == 64) args.counters[tile] = 0;
+          sk_finish<BN>(P, (int)tile, row, v, rs, xch, red);
+        }
       }
+      // phase p done in this CTA: publish (release) for the other CTAs
+      epi_bar();
+      if (threadIdx.x == 64) atom_add_acq_rel(args.phase_ctr + p, 1);
     }
     if (tr && threadIdx.x == 64) tr[4] = gtimer();
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
-  if (tr && threadIdx.x == 0) tr[5] = gtimer();
+  if (threadIdx.x == 0) {
+    // the last CTA to leave resets the phase counters for the next launch
+    if (atom_add_acq_rel(args.phase_ctr + kMaxPhases, 1) == G - 1) {
+      for (int p = 0; p <= kMaxPhases; ++p) args.phase_ctr[p] = 0;
+    }
+    if (tr) tr[5] = gtimer();
+  }
 }
 
 __global__ void rope_table_kernel(const int32_t* __restrict__ pos, int T, int half, float theta,
@@ -854,35 +940,36 @@ SkPlan sk_plan(int M, int N, int K) {
   p.tiles = (N + kBM - 1) / kBM;
   p.kbs = (K + kBK - 1) / kBK;
   p.units = (long long)p.tiles * p.kbs;
-  p.grid = (int)std::min<long long>(num_sms(), p.units);
+  p.grid = num_sms();
   p.maxseg = (p.grid + p.tiles - 1) / p.tiles + 1;
   return p;
 }
 
-// Workspace layout: a fixed counter region shared by every GEMM shape (so
-// GEMMs of different tile counts reuse one workspace in stream order without
-// clobbering each other's counters), then the fp32 partials.
+// Workspace layout: a fixed tile-counter region shared by every GEMM shape
+// (so GEMMs of different tile counts reuse one workspace in stream order
+// without clobbering each other's counters), the phase counters, then the
+// fp32 partials of split tiles.
 constexpr size_t kCounterBytes = 16384 * sizeof(int);
+constexpr size_t kPhaseBytes = 256;
 
-size_t sk_ws_bytes(int M, const SkPlan& p) {
-  return kCounterBytes + (size_t)p.tiles * p.maxseg * M * kBM * sizeof(float);
-}
+size_t partial_bytes(int M, const SkPlan& p) { return (size_t)p.tiles * p.maxseg * M * kBM * sizeof(float); }
 
-// Two CTAs fit per SM (~110 KB each), so the next GEMM's CTA becomes resident
-// and prefetches its weights (PDL) while this one drains.
 template <int BN>
 constexpr size_t sk_extra_bytes() {
   return (size_t)BN * kBM * 2 + 5 * BN * sizeof(float) + 64;
 }
-template <int BN>
+// Single GEMMs: ~104 KB so two CTAs fit per SM and the next kernel's CTA can
+// become resident and prefetch its weights (PDL) while this one drains.
+// Chains: one deep ring per SM (~200 KB), the phases hide each other's tails.
+template <int BN, bool DEEP>
 constexpr int sk_stages() {
-  return (int)((104 * 1024 - sk_extra_bytes<BN>()) / (kBM * kBK * 2 + BN * kBK * 2));
+  return (int)(((DEEP ? 200 : 104) * 1024 - sk_extra_bytes<BN>()) / (kBM * kBK * 2 + BN * kBK * 2));
 }
 
-template <int BN>
-int launch_sk(const CUtensorMap& mw, const CUtensorMap& mx, const SkArgs& a, cudaStream_t st) {
-  constexpr int S = sk_stages<BN>();
-  auto kern = gemm_streamk_kernel<BN, S>;
+template <int BN, bool DEEP>
+int launch_chain(const ChainMaps& maps, const ChainArgs& a, cudaStream_t st) {
+  constexpr int S = sk_stages<BN, DEEP>();
+  auto kern = gemm_chain_kernel<BN, S, DEEP ? 1 : 2>;
   constexpr size_t smem = 1024 + (size_t)S * (kBM * kBK * 2 + BN * kBK * 2) + (2 * S + 4) * 8 + 16 +
                           sk_extra_bytes<BN>();
   static bool attr = false;
@@ -890,7 +977,7 @@ int launch_sk(const CUtensorMap& mw, const CUtensorMap& mx, const SkArgs& a, cud
     ASTRAEA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  ASTRAEA_TRY(launch_k(kern, dim3(a.grid), dim3(kThreads), smem, st, mw, mx, a));
+  ASTRAEA_TRY(launch_k(kern, dim3(a.grid), dim3(kThreads), smem, st, maps, a));
   return 0;
 }
 
@@ -955,9 +1042,80 @@ extern "C" int astraea_rope_table(const int32_t* positions, int32_t T, int32_t h
   return ASTRAEA_OK;
 }
 
+static size_t chain_ws_bytes(int M, int nph, const astraea_gemm_phase* ph) {
+  size_t part = 0;
+  for (int p = 0; p < nph; ++p) part = std::max(part, partial_bytes(M, sk_plan(M, ph[p].N, ph[p].K)));
+  return kCounterBytes + kPhaseBytes + part;
+}
+
 extern "C" size_t astraea_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K) {
   if (M <= 0 || M > kColsMaxM || N <= 0 || K <= 0) return 0;
-  return sk_ws_bytes(M, sk_plan(M, N, K));
+  return kCounterBytes + kPhaseBytes + partial_bytes(M, sk_plan(M, N, K));
+}
+
+extern "C" size_t astraea_gemm_chain_workspace_bytes(int32_t M, int32_t nphases, const astraea_gemm_phase* phases) {
+  if (M <= 0 || M > kColsMaxM || nphases <= 0 || nphases > kMaxPhases || !phases) return 0;
+  return chain_ws_bytes(M, nphases, phases);
+}
+
+// Build and launch a chain of 1..kMaxPhases decode GEMMs (M <= 64 tokens).
+static int run_chain(int M, int nph, const astraea_gemm_phase* ph, void* ws, size_t ws_bytes, bool deep,
+                     cudaStream_t st) {
+  if (M <= 0 || M > kColsMaxM || nph <= 0 || nph > kMaxPhases) return ASTRAEA_EINVAL;
+  if (!ws || ws_bytes < chain_ws_bytes(M, nph, ph)) return ASTRAEA_EINVAL;
+  ChainMaps maps;
+  ChainArgs a;
+  a.trace = nullptr;
+  if (g_trace && g_trace_slots > 0) {
+    a.trace = g_trace + (size_t)(g_trace_next % g_trace_slots) * g_trace_stride;
+    ++g_trace_next;
+  }
+  a.counters = (int*)ws;
+  a.phase_ctr = (int*)((char*)ws + kCounterBytes);
+  a.ws = (float*)((char*)ws + kCounterBytes + kPhaseBytes);
+  a.M = M;
+  a.grid = num_sms();
+  a.nph = nph;
+  const int bn = M <= 16 ? 16 : (M <= 32 ? 32 : 64);
+  for (int p = 0; p < nph; ++p) {
+    const astraea_gemm_phase& q = ph[p];
+    if (q.N <= 0 || q.K <= 0 || q.lda < q.K || q.ldw < q.K || (q.lda % 8) || (q.ldw % 8) || (q.N % 8))
+      return ASTRAEA_EINVAL;
+    Epi e;
+    int rc = to_epi(&q.epi, q.N, &e);
+    if (rc) return rc;
+    const int out_cols = e.kind == EPI_SILU ? q.N / 2 : (e.kind == EPI_QKV_ROPE ? e.Hq * e.D : q.N);
+    if ((q.C && (q.ldc < out_cols || (q.ldc % 8))) || (!q.C && e.kind != EPI_ARGMAX)) return ASTRAEA_EINVAL;
+    const SkPlan pl = sk_plan(M, q.N, q.K);
+    if ((size_t)pl.tiles * sizeof(int) > kCounterBytes) return ASTRAEA_EUNSUPPORTED;
+    SkPhase& P = a.ph[p];
+    P.C = (bf16*)q.C;
+    P.M = M;
+    P.N = q.N;
+    P.K = q.K;
+    P.ldc = q.ldc;
+    P.tiles = pl.tiles;
+    P.kbs = pl.kbs;
+    P.maxseg = pl.maxseg;
+    P.units = pl.units;
+    P.epi = e;
+    if ((rc = make_map(&maps.w[p], q.W, q.N, q.K, q.ldw, kBM))) return rc;
+    if ((rc = make_map(&maps.x[p], q.A, M, q.K, q.lda, bn))) return rc;
+  }
+  if (deep) {
+    if (bn == 16) return launch_chain<16, true>(maps, a, st);
+    if (bn == 32) return launch_chain<32, true>(maps, a, st);
+    return launch_chain<64, true>(maps, a, st);
+  }
+  if (bn == 16) return launch_chain<16, false>(maps, a, st);
+  if (bn == 32) return launch_chain<32, false>(maps, a, st);
+  return launch_chain<64, false>(maps, a, st);
+}
+
+extern "C" int astraea_gemm_chain(int32_t M, int32_t nphases, const astraea_gemm_phase* phases, void* ws,
+                                  size_t ws_bytes, void* stream) {
+  if (!phases) return ASTRAEA_EINVAL;
+  return run_chain(M, nphases, phases, ws, ws_bytes, true, (cudaStream_t)stream);
 }
 
 extern "C" int astraea_gemm_bf16_ex(const void* A, int32_t lda, const void* W, int32_t ldw, void* C, int32_t ldc,
@@ -973,36 +1131,20 @@ extern "C" int astraea_gemm_bf16_ex(const void* A, int32_t lda, const void* W, i
   if (!C && e.kind != EPI_ARGMAX) return ASTRAEA_EINVAL;
   if (M == 0) return ASTRAEA_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  CUtensorMap ma, mb;
   if (M <= kColsMaxM) {
-    const SkPlan p = sk_plan(M, N, K);
-    if (!ws || ws_bytes < sk_ws_bytes(M, p)) return ASTRAEA_EINVAL;
-    if ((size_t)p.tiles * sizeof(int) > kCounterBytes) return ASTRAEA_EUNSUPPORTED;
-    SkArgs a;
-    a.trace = nullptr;
-    if (g_trace && g_trace_slots > 0) {
-      a.trace = g_trace + (size_t)(g_trace_next % g_trace_slots) * g_trace_stride;
-      ++g_trace_next;
-    }
-    a.C = (bf16*)C;
-    a.counters = (int*)ws;
-    a.ws = (float*)((char*)ws + kCounterBytes);
-    a.M = M;
-    a.N = N;
-    a.K = K;
-    a.ldc = ldc;
-    a.tiles = p.tiles;
-    a.kbs = p.kbs;
-    a.grid = p.grid;
-    a.maxseg = p.maxseg;
-    a.units = p.units;
-    a.epi = e;
-    if ((rc = make_map(&ma, W, N, K, ldw, kBM))) return rc;
-    if ((rc = make_map(&mb, A, M, K, lda, p.bn))) return rc;
-    if (p.bn == 16) return launch_sk<16>(ma, mb, a, st);
-    if (p.bn == 32) return launch_sk<32>(ma, mb, a, st);
-    return launch_sk<64>(ma, mb, a, st);
+    astraea_gemm_phase ph;
+    ph.A = A;
+    ph.lda = lda;
+    ph.W = W;
+    ph.ldw = ldw;
+    ph.C = C;
+    ph.ldc = ldc;
+    ph.N = N;
+    ph.K = K;
+    ph.epi = epi ? *epi : astraea_epilogue{};
+    return run_chain(M, 1, &ph, ws, ws_bytes, false, st);
   }
+  CUtensorMap ma, mb;
   GemmArgs a;
   a.C = (bf16*)C;
   a.M = M;

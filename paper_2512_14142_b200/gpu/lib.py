@@ -56,6 +56,22 @@ class Epilogue(ctypes.Structure):
     ]
 
 
+class GemmPhase(ctypes.Structure):
+    """astraea_gemm_phase (include/astraea_b200.h)."""
+
+    _fields_ = [
+        ("A", ctypes.c_void_p),
+        ("lda", ctypes.c_int32),
+        ("W", ctypes.c_void_p),
+        ("ldw", ctypes.c_int32),
+        ("C", ctypes.c_void_p),
+        ("ldc", ctypes.c_int32),
+        ("N", ctypes.c_int32),
+        ("K", ctypes.c_int32),
+        ("epi", Epilogue),
+    ]
+
+
 EPI_SILU = 2
 EPI_QKV_ROPE = 3
 EPI_ARGMAX = 4
@@ -95,6 +111,8 @@ SIGNATURES = {
         ctypes.c_int, [_vp, _i32, _vp, _i32, _vp, _i32, _i32, _i32, _i32, ctypes.POINTER(Epilogue), _vp, _sz, _vp]),
     "astraea_debug_gemm_trace": (ctypes.c_int, [_vp, _i32, _i32]),
     "astraea_rope_table": (ctypes.c_int, [_vp, _i32, _i32, _f32, _vp, _vp]),
+    "astraea_gemm_chain_workspace_bytes": (_sz, [_i32, _i32, ctypes.POINTER(GemmPhase)]),
+    "astraea_gemm_chain": (ctypes.c_int, [_i32, _i32, ctypes.POINTER(GemmPhase), _vp, _sz, _vp]),
     "astraea_decode_advance": (
         ctypes.c_int, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp]),
     "astraea_rmsnorm": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _f32, _vp]),

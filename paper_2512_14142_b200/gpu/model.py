@@ -174,6 +174,7 @@ class LlamaRunner:
                   (cfg.vocab, d)]
         lib = L.load()
         need = max(lib.astraea_gemm_workspace_bytes(64, n, k) for n, k in shapes)
+        # (a chain's workspace is the max over its phases: the same bound)
         # split-K workspace (partials + arrival counters): zero-filled once,
         # the kernel resets its counters.
         self.gemm_ws = torch.zeros(need // 4 + 64, dtype=torch.float32, device=dev)
@@ -262,7 +263,57 @@ class LlamaRunner:
 
     def decode(self, tokens, positions, slots, table, ctx, stream=None, want_logits=False, keys_out=None):
         """One decode step for B rows (retired rows: slot -1, ctx 0). With
-        ``keys_out`` the sampled tokens stay on the device as argmax keys."""
+        ``keys_out`` the sampled tokens stay on the device as argmax keys.
+
+        Launches: embedding, RoPE table, layer 0's QKV GEMM, then per layer
+        the paged attention and ONE chained GEMM kernel running O-proj ->
+        gate/up -> down -> next layer's QKV (the last layer's chain ends
+        with lm_head + argmax instead) -- 2 launches per layer."""
+        if want_logits or self.cfg.num_layers < 1 or tokens.shape[0] > 64:
+            return self._decode_unchained(tokens, positions, slots, table, ctx, stream, want_logits, keys_out)
+        cfg, w, pool = self.cfg, self.w, self.pool
+        B = tokens.shape[0]
+        dev = tokens.device
+        x, ssq0 = self._embed(tokens, stream)
+        dws = self._dec_ws(B, table.shape[1])
+        qd = cfg.num_q_heads * cfg.head_dim
+        d, eps = cfg.hidden, cfg.eps
+        ws = self.gemm_ws
+        q = torch.empty(B, qd, dtype=torch.bfloat16, device=dev)
+        att = torch.empty(B, qd, dtype=torch.bfloat16, device=dev)
+        h = torch.empty(B, cfg.ffn, dtype=torch.bfloat16, device=dev)
+        ssq_mid = torch.empty(self.parts, B, dtype=torch.float32, device=dev)
+        ssq = torch.empty(self.parts, B, dtype=torch.float32, device=dev)
+        keys = keys_out if keys_out is not None else torch.zeros(B, dtype=torch.int64, device=dev)
+        cs = ops.rope_table(positions, cfg.head_dim, cfg.rope_theta, stream=stream)
+
+        def qkv(li, ssq_in):
+            return dict(a=x, w=w.layers[li]["wqkv"], out=q, kind=L.EPI_QKV_ROPE, ssq_in=ssq_in, rms_dim=d,
+                        rms_eps=eps, pool=pool.data, geo=pool.geo, layer=li, num_q_heads=cfg.num_q_heads,
+                        positions=positions, slots=slots, rope_theta=cfg.rope_theta, rope_table=cs)
+
+        ops.gemm_ex(**qkv(0, ssq0), workspace=ws, stream=stream)
+        for li, lw in enumerate(w.layers):
+            ops.decode_attention(pool.geo, pool.data, li, q, qd, B, cfg.num_q_heads, table, ctx, self.scale,
+                                 att, dws, stream=stream)
+            phases = [
+                dict(a=att, w=lw["wo"], out=x, kind=L.EPI_RESIDUAL, residual=x, ssq_out=ssq_mid),
+                dict(a=x, w=lw["wgu"], out=h, kind=L.EPI_SILU, ssq_in=ssq_mid, rms_dim=d, rms_eps=eps),
+                dict(a=h, w=lw["wdown"], out=x, kind=L.EPI_RESIDUAL, residual=x, ssq_out=ssq),
+            ]
+            if li + 1 < cfg.num_layers:
+                phases.append(qkv(li + 1, ssq))
+            else:
+                phases.append(dict(a=x, w=w.lm_head, out=None, kind=L.EPI_ARGMAX, ssq_in=ssq, rms_dim=d, rms_eps=eps,
+                                   argmax_keys=keys))
+            ops.gemm_chain(phases, ws, stream=stream)
+        if keys_out is not None:
+            return keys_out
+        return ops.keys_to_ids(keys)
+
+    def _decode_unchained(self, tokens, positions, slots, table, ctx, stream=None, want_logits=False,
+                          keys_out=None):
+        """Same step, one launch per GEMM (reference path for the chained one)."""
         cfg = self.cfg
         B = tokens.shape[0]
         x, ssq = self._embed(tokens, stream)

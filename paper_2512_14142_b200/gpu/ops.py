@@ -55,6 +55,55 @@ def gemm(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None,
     return out
 
 
+def _epilogue(kind=L.EPI_NONE, residual=None, ssq_out=None, ssq_in=None, rms_dim=0, rms_eps=1e-5, pool=None,
+              geo=None, layer=0, num_q_heads=0, positions=None, slots=None, rope_theta=0.0, rope_table=None,
+              argmax_keys=None):
+    e = L.Epilogue()
+    e.kind = kind
+    e.residual_dev = L.ptr(residual)
+    e.ssq_out_dev = L.ptr(ssq_out)
+    e.ssq_in_dev = L.ptr(ssq_in)
+    e.ssq_in_parts = 0 if ssq_in is None else ssq_in.shape[0]
+    e.rms_dim = rms_dim
+    e.rms_eps = rms_eps
+    e.argmax_keys_dev = L.ptr(argmax_keys)
+    if kind == L.EPI_QKV_ROPE:
+        e.pool_dev = L.ptr(pool)
+        e.geo = geo
+        e.layer = layer
+        e.num_q_heads = num_q_heads
+        e.positions_dev = L.ptr(positions)
+        e.slots_dev = L.ptr(slots)
+        e.rope_theta = rope_theta
+        e.rope_table_dev = L.ptr(rope_table)
+    return e
+
+
+def gemm_chain(phases, workspace, stream=None):
+    """Dependent decode GEMMs in one persistent launch (astraea_gemm_chain).
+
+    ``phases``: list of dicts with a, w, out and the ``gemm_ex`` epilogue
+    keywords; every ``a`` has the same number of rows (M <= 64)."""
+    lib = L.require_cuda()
+    n = len(phases)
+    arr = (L.GemmPhase * n)()
+    M = phases[0]["a"].shape[0]
+    for i, ph in enumerate(phases):
+        a, w, out = ph["a"], ph["w"], ph.get("out")
+        assert a.shape[0] == M
+        q = arr[i]
+        q.A, q.lda = L.ptr(a), a.stride(0)
+        q.W, q.ldw = L.ptr(w), w.stride(0)
+        q.C, q.ldc = L.ptr(out), (out.stride(0) if out is not None else 0)
+        q.N, q.K = w.shape[0], a.shape[1]
+        q.epi = _epilogue(**{k: v for k, v in ph.items() if k not in ("a", "w", "out")})
+    need = lib.astraea_gemm_chain_workspace_bytes(M, n, arr)
+    assert workspace.numel() * workspace.element_size() >= need, "chain workspace too small"
+    L.check(lib.astraea_gemm_chain(M, n, arr, L.ptr(workspace), workspace.numel() * workspace.element_size(),
+                                   _s(stream)), "gemm_chain")
+    _count()
+
+
 def gemm_ex(a, w, out, kind=L.EPI_NONE, residual=None, ssq_out=None, ssq_in=None, rms_dim=0, rms_eps=1e-5,
             pool=None, geo=None, layer=0, num_q_heads=0, positions=None, slots=None, rope_theta=0.0,
             rope_table=None, argmax_keys=None, workspace=None, stream=None):

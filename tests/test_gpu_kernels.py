@@ -409,3 +409,43 @@ def test_gemm_qkv_rope_append(M, Hq, Hkv, D):
     assert rel_err(ks, k_ref[1:]) < 1e-2 and rel_err(vs, v_ref[1:]) < 1e-2
     first = blocks[50 // 16] * 16 + 50 % 16
     assert torch.count_nonzero(p6[first // 16, 1, :, :, first % 16]) == 0   # slot -1 skipped
+
+
+@pytest.mark.parametrize("M", [1, 3, 20, 64])
+def test_gemm_chain_equals_separate_gemms(M):
+    """O -> gate/up -> down -> lm_head argmax, chained vs one launch each."""
+    from paper_2512_14142_b200.gpu.model import interleave_gate_up
+    d, F, V = 512, 1536, 4096
+    g = torch.Generator(device=DEV).manual_seed(M)
+    att = torch.randn(M, d, generator=g, device=DEV).bfloat16()
+    x0 = torch.randn(M, d, generator=g, device=DEV).bfloat16()
+    wo = (torch.randn(d, d, generator=g, device=DEV) * 0.05).bfloat16()
+    wgu = interleave_gate_up((torch.randn(2 * F, d, generator=g, device=DEV) * 0.05).bfloat16(), F).contiguous()
+    wd = (torch.randn(d, F, generator=g, device=DEV) * 0.05).bfloat16()
+    wl = (torch.randn(V, d, generator=g, device=DEV) * 0.05).bfloat16()
+    ws = torch.zeros(64 << 20, dtype=torch.float32, device=DEV)
+    outs = {}
+    for chained in (False, True):
+        x = x0.clone()
+        h = torch.empty(M, F, dtype=torch.bfloat16, device=DEV)
+        s1 = torch.empty(d // 128, M, dtype=torch.float32, device=DEV)
+        s2 = torch.empty_like(s1)
+        keys = torch.zeros(M, dtype=torch.int64, device=DEV)
+        ph = [dict(a=att, w=wo, out=x, kind=L.EPI_RESIDUAL, residual=x, ssq_out=s1),
+              dict(a=x, w=wgu, out=h, kind=L.EPI_SILU, ssq_in=s1, rms_dim=d, rms_eps=1e-5),
+              dict(a=h, w=wd, out=x, kind=L.EPI_RESIDUAL, residual=x, ssq_out=s2),
+              dict(a=x, w=wl, out=None, kind=L.EPI_ARGMAX, ssq_in=s2, rms_dim=d, rms_eps=1e-5, argmax_keys=keys)]
+        for _ in range(2):   # twice: the phase counters must reset between launches
+            x.copy_(x0)
+            keys.zero_()
+            if chained:
+                ops.gemm_chain(ph, ws)
+            else:
+                for p in ph:
+                    kw = {k: v for k, v in p.items() if k not in ("a", "w", "out")}
+                    ops.gemm_ex(p["a"], p["w"], p["out"], workspace=ws, **kw)
+        torch.cuda.synchronize()
+        outs[chained] = (x.clone(), h.clone(), keys.clone())
+    assert torch.equal(outs[True][0], outs[False][0])
+    assert torch.equal(outs[True][1], outs[False][1])
+    assert torch.equal(outs[True][2], outs[False][2])

@@ -120,3 +120,32 @@ def test_kv_action_invariance_preserve_swap_discard():
     kv_d = d[1].view(torch.bfloat16).float()
     assert float((kv_p - kv_d).norm() / kv_p.norm()) < 1e-2   # recompute: within tolerance
     assert p[2][:49] == d[2][:49]                              # segment-1 context re-fed exactly
+
+
+@pytest.mark.parametrize("B", [1, 4])
+def test_chained_decode_step_equals_unchained(B):
+    """The 2-launches-per-layer decode step is bit-identical to the
+    one-launch-per-GEMM step (same tokens, same KV written)."""
+    cfg = PRESETS["small"]
+    w = LlamaWeights(cfg, seed=4)
+    d = lambda v: torch.tensor(v, dtype=torch.int32, device=DEV)  # noqa: E731
+    results = []
+    for chained in (True, False):
+        pool = KvPool(cfg, 64)
+        runner = LlamaRunner(w, pool)
+        for b in range(B):
+            ids = segment_token_ids(f"c{b}", 1, 20 + b, cfg.vocab)
+            _prefill_one(runner, pool, ids, [4 * b, 4 * b + 1, 4 * b + 2, 4 * b + 3])
+        toks = d([7 + b for b in range(B)])
+        pos = d([20 + b for b in range(B)])
+        table = d([[4 * b, 4 * b + 1, 4 * b + 2, 4 * b + 3] for b in range(B)])
+        slots = d([4 * b * 16 + 16 + (20 + b) % 16 for b in range(B)])
+        ctx = d([21 + b for b in range(B)])
+        if chained:
+            out = runner.decode(toks, pos, slots, table, ctx)
+        else:
+            out = runner._decode_unchained(toks, pos, slots, table, ctx)
+        torch.cuda.synchronize()
+        results.append((out.cpu(), pool.data.clone()))
+    assert torch.equal(results[0][0], results[1][0])
+    assert torch.equal(results[0][1], results[1][1])
