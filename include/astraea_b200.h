@@ -260,10 +260,11 @@ ASTRAEA_API int astraea_gemm_bf16_ex(const void* A_dev, int32_t lda, const void*
                          const astraea_epilogue* epilogue, void* workspace_dev,
                          size_t workspace_bytes, void* stream);
 
-/* Diagnostics: when buf != NULL, each following decode (stream-K) GEMM launch
- * writes per-CTA %globaltimer stamps [grid][8] into the next of `slots` slots
- * of `slot_stride` u64 each (entry, dependency released, first stage, last
- * MMA issued, epilogue done, exit). Pass NULL to disable. */
+/* Diagnostics: when buf != NULL, each following decode (stream-K / chain)
+ * GEMM launch writes per-CTA %globaltimer stamps [grid][16] into the next of
+ * `slots` slots of `slot_stride` u64 each: [0] entry, [1+p] activations of
+ * phase p released, [5+p] epilogue of phase p done, [9] MMAs done, [10] exit.
+ * Pass NULL to disable. */
 ASTRAEA_API int astraea_debug_gemm_trace(void* buf, int32_t slots, int32_t slot_stride);
 
 /* RoPE angle table for a batch: table[t][i] = (cos, sin)(positions[t] * theta^(-2i/D)),

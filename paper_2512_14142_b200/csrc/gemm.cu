@@ -470,9 +470,20 @@ struct SkPhase {
   bf16* C;
   int M, N, K, ldc;
   int tiles, kbs, maxseg;
+  int geff;          // CTAs sharing this phase's units: min(grid, units); the rest idle in it
   long long units;
   Epi epi;
 };
+
+// Stream-K range of CTA `cta` in a phase: [u0, u1) (empty for cta >= geff).
+__device__ __forceinline__ void sk_range(const SkPhase& P, int cta, long long& u0, long long& u1) {
+  if (cta < P.geff) {
+    u0 = (long long)cta * P.units / P.geff;
+    u1 = (long long)(cta + 1) * P.units / P.geff;
+  } else {
+    u0 = u1 = P.units;
+  }
+}
 
 struct ChainMaps {
   CUtensorMap w[kMaxPhases];
@@ -626,7 +637,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
   const int G = args.grid;
-  unsigned long long* tr = args.trace ? args.trace + (long long)cta * 8 : nullptr;
+  unsigned long long* tr = args.trace ? args.trace + (long long)cta * 16 : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = gtimer();
 
   if (warp == 0 && lane == 0) {
@@ -657,7 +668,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
       for (int p = 0; p < args.nph; ++p) {
         const SkPhase& P = args.ph[p];
         const int KB = P.kbs;
-        const long long u0 = (long long)cta * P.units / G, u1 = (long long)(cta + 1) * P.units / G;
+        long long u0, u1;
+        sk_range(P, cta, u0, u1);
         const int pre = (int)(u1 - u0 < STAGES ? u1 - u0 : STAGES);
         // weights first: independent of the previous phase / kernel
         for (int k = 0; k < pre; ++k) {
@@ -673,7 +685,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
           wait_phase(args.phase_ctr + p - 1, G);
           asm volatile("fence.proxy.async;" ::: "memory");   // generic-proxy writes -> TMA reads
         }
-        if (tr && p == 0) tr[1] = gtimer();
+        if (tr) tr[1 + p] = gtimer();   // activations of phase p released
         for (int k = 0; k < pre; ++k) {
           const int s = (i + k) % STAGES;
           tma_load_2d(sb + s * B_BYTES, &maps.x[p], &full[s], (int)((u0 + k) % KB) * kBK, 0);
@@ -697,7 +709,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
     for (int p = 0; p < args.nph; ++p) {
       const SkPhase& P = args.ph[p];
       const int KB = P.kbs;
-      const long long u0 = (long long)cta * P.units / G, u1 = (long long)(cta + 1) * P.units / G;
+      long long u0, u1;
+      sk_range(P, cta, u0, u1);
       for (long long u = u0; u < u1; ++seg) {
         const long long tile = u / KB;
         const long long seg_end = min(u1, (tile + 1) * KB);
@@ -711,7 +724,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
           mbar_wait(&full[s], (i / STAGES) & 1);
           tc_fence_after();
           if (lane == 0) {
-            if (tr && i == 0) tr[2] = gtimer();
+
             const uint64_t da = smem_desc_sw128(sa + s * A_BYTES);
             const uint64_t db = smem_desc_sw128(sb + s * B_BYTES);
 #pragma unroll
@@ -725,7 +738,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         __syncwarp();
       }
     }
-    if (tr && lane == 0) tr[3] = gtimer();
+    if (tr && lane == 0) tr[9] = gtimer();
   } else {
     pdl_wait();
     const int quarter = warp & 3;
@@ -736,7 +749,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
       const SkPhase& P = args.ph[p];
       const int KB = P.kbs;
       const long long U = P.units;
-      const long long u0 = (long long)cta * U / G, u1 = (long long)(cta + 1) * U / G;
+      long long u0, u1;
+      sk_range(P, cta, u0, u1);
       // Everything this phase's epilogue reads from earlier phases (residual,
       // norm statistics) was published by those phases' barrier: acquire it
       // once, then order the other epilogue threads behind it.
@@ -767,8 +781,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
           continue;
         }
         const long long first_u = tile * KB;
-        const int c_first = sk_owner(first_u, U, G);
-        const int nseg = sk_owner(first_u + KB - 1, U, G) - c_first + 1;
+        const int c_first = sk_owner(first_u, U, P.geff);
+        const int nseg = sk_owner(first_u + KB - 1, U, P.geff) - c_first + 1;
         const int sidx = cta - c_first;
         float* part = args.ws + ((tile * P.maxseg + sidx) * (long long)args.M) * kBM;
 #pragma unroll
@@ -822,9 +836,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
       }
       // phase p done in this CTA: publish (release) for the other CTAs
       epi_bar();
-      if (threadIdx.x == 64) atom_add_acq_rel(args.phase_ctr + p, 1);
+      if (threadIdx.x == 64) {
+        atom_add_acq_rel(args.phase_ctr + p, 1);
+        if (tr) tr[5 + p] = gtimer();
+      }
     }
-    if (tr && threadIdx.x == 64) tr[4] = gtimer();
   }
   tc_fence_before();
   __syncthreads();
@@ -834,7 +850,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     if (atom_add_acq_rel(args.phase_ctr + kMaxPhases, 1) == G - 1) {
       for (int p = 0; p <= kMaxPhases; ++p) args.phase_ctr[p] = 0;
     }
-    if (tr) tr[5] = gtimer();
+    if (tr) tr[10] = gtimer();
   }
 }
 
@@ -1098,6 +1114,7 @@ static int run_chain(int M, int nph, const astraea_gemm_phase* ph, void* ws, siz
     P.kbs = pl.kbs;
     P.maxseg = pl.maxseg;
     P.units = pl.units;
+    P.geff = (int)std::min<long long>(a.grid, pl.units);
     P.epi = e;
     if ((rc = make_map(&maps.w[p], q.W, q.N, q.K, q.ldw, kBM))) return rc;
     if ((rc = make_map(&maps.x[p], q.A, M, q.K, q.lda, bn))) return rc;

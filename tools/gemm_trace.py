@@ -1,8 +1,9 @@
-"""Per-CTA timeline of the decode (stream-K) GEMMs of one layer, from
-%globaltimer stamps (astraea_debug_gemm_trace). Runs a layer's 4 GEMMs
-back to back a few times (PDL chain) and reports, per GEMM, the spread of
-CTA entry, dependency release, first MMA, last MMA, epilogue end and exit,
-relative to the previous GEMM's last exit."""
+"""Per-CTA timeline of the decode GEMM chain of one layer (O -> GU -> Down ->
+next QKV) from %globaltimer stamps (astraea_debug_gemm_trace).
+
+For each phase: when its activations were released to the producer
+(phase barrier / PDL), and when each CTA's epilogue finished the phase,
+as [min, median, max] microseconds after the chain's first CTA entry."""
 import json
 import sys
 from pathlib import Path
@@ -22,46 +23,54 @@ pool = KvPool(cfg, 64)
 r = LlamaRunner(w, pool)
 dev = "cuda"
 d, F, qd = cfg.hidden, cfg.ffn, cfg.num_q_heads * cfg.head_dim
-lw = w.layers[0]
+lw, lw1 = w.layers[0], w.layers[1]
 ws = r.gemm_ws
 x = torch.randn(B, d, device=dev).bfloat16()
 att = torch.randn(B, qd, device=dev).bfloat16()
-h = torch.randn(B, F, device=dev).bfloat16()
-q = torch.empty(B, cfg.qkv_dim, device=dev).bfloat16()
-ssq = (x.float().pow(2).view(B, -1, 128).sum(-1)).T.contiguous()
-ssq2 = torch.empty_like(ssq)
-gu = torch.empty(B, F, device=dev).bfloat16()
-seq = [("qkv", lambda: ops.gemm(x, lw["wqkv"], out=q, workspace=ws)),
-       ("o", lambda: ops.gemm_ex(att, lw["wo"], x, kind=L.EPI_RESIDUAL, residual=x, ssq_out=ssq2, workspace=ws)),
-       ("gu", lambda: ops.gemm_ex(x, lw["wgu"], gu, kind=L.EPI_SILU, ssq_in=ssq2, rms_dim=d, rms_eps=1e-5, workspace=ws)),
-       ("down", lambda: ops.gemm_ex(h, lw["wdown"], x, kind=L.EPI_RESIDUAL, residual=x, ssq_out=ssq, workspace=ws))]
-reps = 3
-for _ in range(2):
-    for _, f in seq:
-        f()
+h = torch.empty(B, F, device=dev).bfloat16()
+q = torch.empty(B, qd, device=dev).bfloat16()
+s1 = torch.empty(d // 128, B, device=dev)
+s2 = torch.empty(d // 128, B, device=dev)
+pos = torch.full((B,), 100, dtype=torch.int32, device=dev)
+slots = torch.arange(B, dtype=torch.int32, device=dev)
+cs = ops.rope_table(pos, cfg.head_dim, cfg.rope_theta)
+phases = [dict(a=att, w=lw["wo"], out=x, kind=L.EPI_RESIDUAL, residual=x, ssq_out=s1),
+          dict(a=x, w=lw["wgu"], out=h, kind=L.EPI_SILU, ssq_in=s1, rms_dim=d, rms_eps=cfg.eps),
+          dict(a=h, w=lw["wdown"], out=x, kind=L.EPI_RESIDUAL, residual=x, ssq_out=s2),
+          dict(a=x, w=lw1["wqkv"], out=q, kind=L.EPI_QKV_ROPE, ssq_in=s2, rms_dim=d, rms_eps=cfg.eps,
+               pool=pool.data, geo=pool.geo, layer=1, num_q_heads=cfg.num_q_heads, positions=pos, slots=slots,
+               rope_theta=cfg.rope_theta, rope_table=cs)]
+for _ in range(3):
+    ops.gemm_chain(phases, ws)
 torch.cuda.synchronize()
+reps = 3
 lib = L.load()
-buf = torch.zeros(reps * len(seq), 148 * 8, dtype=torch.int64, device=dev)
-lib.astraea_debug_gemm_trace(buf.data_ptr(), reps * len(seq), 148 * 8)
+buf = torch.zeros(reps, 148 * 16, dtype=torch.int64, device=dev)
+lib.astraea_debug_gemm_trace(buf.data_ptr(), reps, 148 * 16)
 for _ in range(reps):
-    for _, f in seq:
-        f()
+    ops.gemm_chain(phases, ws)
 torch.cuda.synchronize()
 lib.astraea_debug_gemm_trace(None, 0, 0)
-t = buf.view(reps * len(seq), 148, 8).cpu().double()
-out = []
-prev_exit = None
-for i in range(reps * len(seq)):
-    name = seq[i % len(seq)][0]
-    s = t[i]
-    base = prev_exit if prev_exit is not None else s[:, 0].min()
-    row = {"gemm": name}
-    for j, lab in enumerate(["entry", "dep", "first_mma", "last_mma", "epi_done", "exit"]):
-        col = s[:, j]
-        col = col[col > 0]
-        if len(col):
-            row[lab] = [round(float(col.min() - base) / 1000, 2), round(float(col.median() - base) / 1000, 2),
-                        round(float(col.max() - base) / 1000, 2)]
-    prev_exit = s[:, 5].max()
-    out.append(row)
-print(json.dumps(out[len(seq):], indent=0))
+t = buf.view(reps, 148, 16).cpu().double()
+names = ["o", "gu", "down", "qkv"]
+
+
+def mmm(col, base):
+    col = col[col > 0]
+    return [round(float(col.min() - base) / 1000, 2), round(float(col.median() - base) / 1000, 2),
+            round(float(col.max() - base) / 1000, 2)]
+
+
+for rr in range(reps):
+    s = t[rr]
+    base = s[:, 0].min()
+    row = {"rep": rr, "entry": mmm(s[:, 0], base)}
+    for p, n in enumerate(names):
+        row[n + "_x_released"] = mmm(s[:, 1 + p], base)
+        row[n + "_epi_done"] = mmm(s[:, 5 + p], base)
+    row["mma_done"] = mmm(s[:, 9], base)
+    row["exit"] = mmm(s[:, 10], base)
+    print(json.dumps(row))
+by = {n: ph["w"].numel() * 2 for n, ph in zip(names, phases)}
+print(json.dumps({"weight_MB": {k: round(v / 1e6, 1) for k, v in by.items()},
+                  "ideal_us_at_6.5TBps": {k: round(v / 6.5e6, 1) for k, v in by.items()}}))
