@@ -371,6 +371,7 @@ class KvDataPath:
                 gb = g["bufs"]
                 gb["step"].zero_()
                 gb["sampled"].zero_()
+                gb["hist"].zero_()      # rows past their n_gen read back as 0, as in the eager path
                 gb["n_gen"][:B].copy_(view("n_gen"))
                 gb["base_pos"][:B].copy_(view("base_pos"))
                 gb["first_tok"][:B].copy_(first_tok)

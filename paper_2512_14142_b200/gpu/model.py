@@ -183,6 +183,7 @@ class LlamaRunner:
         self._old_ws = []
         self.device = dev
         self.parts = -(-d // 128)
+        self.use_chain = True   # decode GEMMs as one persistent chain per layer (False: one launch each)
 
     def _dec_ws(self, B, max_blocks):
         need = L.load().astraea_decode_workspace_bytes(B, self.cfg.num_q_heads, self.cfg.head_dim, max_blocks)
@@ -269,7 +270,7 @@ class LlamaRunner:
         the paged attention and ONE chained GEMM kernel running O-proj ->
         gate/up -> down -> next layer's QKV (the last layer's chain ends
         with lm_head + argmax instead) -- 2 launches per layer."""
-        if want_logits or self.cfg.num_layers < 1 or tokens.shape[0] > 64:
+        if want_logits or not self.use_chain or self.cfg.num_layers < 1 or tokens.shape[0] > 64:
             return self._decode_unchained(tokens, positions, slots, table, ctx, stream, want_logits, keys_out)
         cfg, w, pool = self.cfg, self.w, self.pool
         B = tokens.shape[0]
