@@ -260,6 +260,59 @@ ASTRAEA_API int astraea_gemm_bf16_ex(const void* A_dev, int32_t lda, const void*
                          const astraea_epilogue* epilogue, void* workspace_dev,
                          size_t workspace_bytes, void* stream);
 
+/* ---- one decode step as one persistent kernel ------------------------------------------------
+ * The whole decode step (every layer's QKV+RoPE+append, paged attention, O,
+ * gate/up+SiLU, down, then lm_head+argmax) as ONE launch over a *program* of
+ * phases, for M <= 64 rows. Phases are ordered; dependencies point backwards
+ * and are tracked per chunk (128-feature GEMM tile, kv head) with epoch flags,
+ * so phases overlap across SMs with no grid-wide barrier while the weight
+ * stream never waits. Replaces the n_gen * seconds_per_token term of
+ * Engine._actual_seconds (simulator.py:329-337) for the decode loop.
+ *   GEMM phase: `gemm` as in astraea_gemm_chain (A rows = M);
+ *     a_from   = phase producing A (-1: A is ready at launch)
+ *     epi_from = phase whose output the epilogue reads (RMS statistics or the
+ *                residual), -1: none / ready at launch
+ *   ATTN phase: paged decode attention of `layer`; q rows at q_dev (row
+ *     stride q_row_stride elements, [Hq][D]); out_dev dense [M][Hq*D];
+ *     qkv_from = the QKV_ROPE GEMM phase that produced q and this step's K/V.
+ * Program: astraea_step_program_bytes(n) bytes; build writes the phase
+ * descriptors into program_host (any host memory, 128-byte aligned), the
+ * caller copies them to a device buffer of the same size (stream-ordered,
+ * e.g. from pinned memory) that astraea_step_launch reads. Workspace:
+ * astraea_step_workspace_bytes(...) bytes of device memory, zero-filled once
+ * before first use; programs built on one workspace may be launched one
+ * after another on one stream, never concurrently. */
+enum { ASTRAEA_PHASE_GEMM = 0, ASTRAEA_PHASE_ATTN = 1 };
+typedef struct {
+  int32_t kind;
+  astraea_gemm_phase gemm;
+  int32_t a_from;
+  int32_t epi_from;
+  const void* pool_dev;
+  astraea_kv_geometry geo;
+  int32_t layer;
+  int32_t num_q_heads;
+  const void* q_dev;
+  int32_t q_row_stride;
+  const int32_t* table_dev;
+  int32_t max_blocks;
+  const int32_t* ctx_dev;
+  float scale;
+  void* out_dev;
+  int32_t qkv_from;
+} astraea_step_phase;
+ASTRAEA_API size_t astraea_step_program_bytes(int32_t nphases);
+ASTRAEA_API size_t astraea_step_workspace_bytes(int32_t M, int32_t nphases, const astraea_step_phase* phases);
+ASTRAEA_API int astraea_step_program_build(int32_t M, int32_t nphases, const astraea_step_phase* phases,
+                               void* program_host, size_t program_bytes, void* workspace_dev,
+                               size_t workspace_bytes);
+/* l2_lookahead: weight tiles per CTA prefetched into L2 ahead of the smem ring (0: off). */
+/* Diagnostics: when buf != NULL, following step launches write %globaltimer
+ * stamps [grid][nphases][4] (+[grid] entry stamps) into buf; NULL disables. */
+ASTRAEA_API int astraea_debug_step_trace(void* buf);
+ASTRAEA_API int astraea_step_launch(int32_t M, int32_t nphases, const void* program_dev, void* workspace_dev,
+                        int32_t l2_lookahead, void* stream);
+
 /* Diagnostics: when buf != NULL, each following decode (stream-K / chain)
  * GEMM launch writes per-CTA %globaltimer stamps [grid][16] into the next of
  * `slots` slots of `slot_stride` u64 each: [0] entry, [1+p] activations of

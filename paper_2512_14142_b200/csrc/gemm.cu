@@ -41,169 +41,14 @@
 #include <unordered_map>
 
 #include "common.cuh"
+#include "tc.cuh"
 
 using namespace astraea;
+using namespace astraea::tc;
 
 namespace {
 
-constexpr int kBM = 128;   // MMA M
-constexpr int kBK = 64;    // K per stage = one 128-byte swizzle atom of bf16
 constexpr int kThreads = 192;
-
-// ---- PTX wrappers -------------------------------------------------------------------
-
-__device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
-          "r"(smem_u32(smem)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
-
-__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t cols) {
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
-               "r"(cols));
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-}
-__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols));
-}
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-
-__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                         uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
-}
-
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-// 32 lanes x 32 consecutive fp32 columns: thread i of the warp gets row (quarter*32 + i).
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups of
-// 1024 bytes (SBO), version 1 (sm_100).
-__device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
-  const uint64_t addr = smem_u32(p);
-  uint64_t d = 0;
-  d |= (addr >> 4) & 0x3FFFull;            // start address
-  d |= (uint64_t)1 << 16;                  // LBO (unused for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;        // SBO
-  d |= (uint64_t)1 << 46;                  // version
-  d |= (uint64_t)2 << 61;                  // SWIZZLE_128B
-  return d;
-}
-
-// Instruction descriptor: D=f32, A=B=bf16, both K-major, M=128, N=n.
-__host__ __device__ constexpr uint32_t instr_desc(int n) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
-}
-
-__device__ __forceinline__ float round_bf(float x) { return bf2f(f2bf(x)); }
-
-__device__ __forceinline__ float silu_rounded(float g) {
-  // silu(g) is materialised in bf16 by the reference formulation
-  return round_bf(g / (1.f + __expf(-g)));
-}
-
-// ---- epilogue program --------------------------------------------------------------
-
-struct Epi {
-  int kind;
-  const bf16* residual;
-  float* ssq_out;          // [ceil(N/128)][M]
-  const float* ssq_in;     // [parts][M]
-  int ssq_parts;
-  int rms_dim;
-  float eps;
-  bf16* pool;
-  long long block_el;
-  int layer, Hq, Hkv, D, bt;
-  const int32_t* pos;
-  const int32_t* slots;
-  float theta;
-  const float2* cs;        // optional [M][D/2] (cos, sin) table
-  unsigned long long* amax;  // ARGMAX: [M] packed (value, index) keys
-};
-
-// Greedy-sampling key: order-preserving float bits in the high word, the
-// complemented column in the low word, so atomicMax picks the largest value
-// and, among equal values, the lowest index (torch.argmax's tie rule).
-__device__ __forceinline__ unsigned long long argmax_key(float x, int col) {
-  const uint32_t b = __float_as_uint(x);
-  const uint32_t u = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-  return ((unsigned long long)u << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)col);
-}
-
-__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
-  return a > b ? a : b;
-}
-
-__device__ __forceinline__ unsigned long long warp_max64(unsigned long long v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = umax64(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-
-// (cos, sin) of token t's rotation for frequency index i (< D/2).
-__device__ __forceinline__ float2 rope_cs(const Epi& e, int t, int i) {
-  if (e.cs) return e.cs[(long long)t * (e.D / 2) + i];
-  float sn, cs;
-  sincosf((float)e.pos[t] * (1.0f / powf(e.theta, (float)(2 * i) / (float)e.D)), &sn, &cs);
-  return make_float2(cs, sn);
-}
-
-__device__ __forceinline__ float rms_scale(const Epi& e, int M, int t) {
-  // independent loads in groups of 8 (the sum order stays p = 0, 1, 2, ...)
-  float s = 0.f;
-  int p = 0;
-  for (; p + 8 <= e.ssq_parts; p += 8) {
-    float v[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = __ldcg(e.ssq_in + (long long)(p + k) * M + t);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) s += v[k];
-  }
-  for (; p < e.ssq_parts; ++p) s += __ldcg(e.ssq_in + (long long)p * M + t);
-  return rsqrtf(s / (float)e.rms_dim + e.eps);
-}
-
-// Destination of a rotated/plain head element in QKV_ROPE: q -> C, k/v -> pool.
-__device__ __forceinline__ void qkv_store(const Epi& e, bf16* C, int ldc, int t, int head, int hrow, float y) {
-  if (head < e.Hq) {
-    C[(long long)t * ldc + head * e.D + hrow] = f2bf(y);
-    return;
-  }
-  const int slot = e.slots[t];
-  if (slot < 0) return;
-  const int kv = head < e.Hq + e.Hkv ? 0 : 1;
-  const int h = head - e.Hq - kv * e.Hkv;
-  const int blk = slot / e.bt, off = slot % e.bt;
-  bf16* base = e.pool + (long long)blk * e.block_el + ((long long)(e.layer * 2 + kv) * e.Hkv + h) * e.bt * e.D;
-  base[(long long)off * e.D + hrow] = f2bf(y);
-}
-
-enum { EPI_NONE = 0, EPI_RESIDUAL = 1, EPI_SILU = 2, EPI_QKV_ROPE = 3, EPI_ARGMAX = 4 };
 
 struct GemmArgs {
   bf16* C;
@@ -499,120 +344,15 @@ struct ChainArgs {
   SkPhase ph[kMaxPhases];
 };
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 __device__ __forceinline__ int sk_owner(long long u, long long units, int grid) {
   return (int)(((u + 1) * grid - 1) / units);
-}
-
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
-
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
-  int prev;
-  asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], %2;" : "=r"(prev) : "l"(p), "r"(v) : "memory");
-  return prev;
 }
 
 __device__ __forceinline__ void wait_phase(const int* ctr, int target) {
   while (ld_acquire(ctr) < target) __nanosleep(32);
 }
 
-
-// Finish one 128-feature tile: thread `row` holds v[t] (t < M) of feature
-// tile*128 + row. All 128 epilogue threads call this together.
-template <int BN, typename A>
-__device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* v, const float* rs,
-                                          bf16* xch, float* red) {
-  const Epi& e = a.epi;
-  const int M = a.M;
-  const int f = tile * kBM + row;
-  const bool fok = f < a.N;
-  if (e.ssq_in) {
-#pragma unroll
-    for (int t = 0; t < BN; ++t) v[t] *= rs[t];
-  }
-  if (e.kind == EPI_ARGMAX) {
-#pragma unroll
-    for (int t = 0; t < BN; ++t) {
-      if (t >= M) break;
-      if (a.C && fok) a.C[(long long)t * a.ldc + f] = f2bf(v[t]);
-      const unsigned long long k = warp_max64(fok ? argmax_key(v[t], f) : 0ull);
-      if ((row & 31) == 0) atomicMax(e.amax + t, k);
-    }
-    return;
-  }
-  if (e.kind == EPI_NONE || e.kind == EPI_RESIDUAL) {
-    float sq[BN];
-#pragma unroll
-    for (int t = 0; t < BN; ++t) {
-      sq[t] = 0.f;
-      if (t < M && fok) {
-        float o = v[t];
-        if (e.kind == EPI_RESIDUAL) o += bf2f(e.residual[(long long)t * a.ldc + f]);
-        const bf16 ob = f2bf(o);
-        a.C[(long long)t * a.ldc + f] = ob;
-        sq[t] = bf2f(ob) * bf2f(ob);
-      }
-    }
-    if (e.ssq_out) {
-      const int q = row >> 5, lane = row & 31;
-#pragma unroll
-      for (int t = 0; t < BN; ++t) {
-        const float s = warp_sum(sq[t]);
-        if (lane == 0) red[q * BN + t] = s;
-      }
-      epi_bar();
-      if (row < M) e.ssq_out[(long long)tile * M + row] = red[row] + red[BN + row] + red[2 * BN + row] + red[3 * BN + row];
-      epi_bar();
-    }
-    return;
-  }
-  // pair exchange through shared memory (values rounded to bf16, as the
-  // unfused formulation materialises them)
-#pragma unroll
-  for (int t = 0; t < BN; ++t) xch[t * kBM + row] = f2bf(v[t]);
-  epi_bar();
-  if (e.kind == EPI_SILU) {
-    if (row >= 64) {
-      const int out_f = tile * 64 + (row - 64);
-      if (fok) {
-#pragma unroll
-        for (int t = 0; t < BN; ++t)
-          if (t < M)
-            a.C[(long long)t * a.ldc + out_f] = f2bf(silu_rounded(bf2f(xch[t * kBM + row - 64])) * bf2f(xch[t * kBM + row]));
-      }
-    }
-  } else {  // QKV_ROPE
-    const int head = f / e.D, hrow = f % e.D, half = e.D / 2;
-    const int partner = row ^ half;
-    const bool rot = head < e.Hq + e.Hkv;
-    if (fok) {
-#pragma unroll 4
-      for (int t = 0; t < BN; ++t) {
-        if (t >= M) break;
-        const float x = bf2f(xch[t * kBM + row]);
-        float y = x;
-        if (rot) {
-          const float xp = bf2f(xch[t * kBM + partner]);
-          const float2 r = rope_cs(e, t, hrow % half);
-          y = hrow < half ? x * r.x - xp * r.y : x * r.x + xp * r.y;
-        }
-        qkv_store(e, a.C, a.ldc, t, head, hrow, y);
-      }
-    }
-  }
-  epi_bar();
-}
 
 template <int BN, int STAGES, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
@@ -868,68 +608,6 @@ __global__ void rope_table_kernel(const int32_t* __restrict__ pos, int T, int ha
 
 // ---- host side ----------------------------------------------------------------------------
 
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  });
-  return fn;
-}
-
-struct MapKey {
-  const void* ptr;
-  long long rows, cols, ld;
-  int box_rows;
-  bool operator==(const MapKey& o) const {
-    return ptr == o.ptr && rows == o.rows && cols == o.cols && ld == o.ld && box_rows == o.box_rows;
-  }
-};
-struct MapKeyHash {
-  size_t operator()(const MapKey& k) const {
-    size_t h = std::hash<const void*>()(k.ptr);
-    h ^= std::hash<long long>()(k.rows * 1315423911ll + k.cols * 2654435761ll + k.ld) + 0x9e3779b9 + (h << 6);
-    return h ^ (size_t)k.box_rows;
-  }
-};
-
-// 2-D bf16 tensor [rows][cols] (row stride ld elements), box = kBK cols x box_rows rows, 128B swizzle.
-int make_map(CUtensorMap* out, const void* ptr, long long rows, long long cols, long long ld, int box_rows) {
-  static std::mutex mu;
-  static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
-  MapKey key{ptr, rows, cols, ld, box_rows};
-  {
-    std::lock_guard<std::mutex> g(mu);
-    auto it = cache.find(key);
-    if (it != cache.end()) {
-      *out = it->second;
-      return 0;
-    }
-  }
-  EncodeTiledFn fn = encode_fn();
-  if (!fn) return ASTRAEA_EUNSUPPORTED;
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-  cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return ASTRAEA_EINVAL;
-  std::lock_guard<std::mutex> g(mu);
-  if (cache.size() > 4096) cache.clear();
-  cache.emplace(key, *out);
-  return 0;
-}
-
 template <int BN, int STAGES>
 int launch_rows(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, dim3 grid, cudaStream_t st) {
   auto kern = gemm_rows_kernel<BN, STAGES>;
@@ -1036,6 +714,73 @@ int to_epi(const astraea_epilogue* in, int N, Epi* e) {
 }
 
 }  // namespace
+
+namespace astraea {
+namespace tc {
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+struct MapKey {
+  const void* ptr;
+  long long rows, cols, ld;
+  int box_rows;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && rows == o.rows && cols == o.cols && ld == o.ld && box_rows == o.box_rows;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    size_t h = std::hash<const void*>()(k.ptr);
+    h ^= std::hash<long long>()(k.rows * 1315423911ll + k.cols * 2654435761ll + k.ld) + 0x9e3779b9 + (h << 6);
+    return h ^ (size_t)k.box_rows;
+  }
+};
+
+// 2-D bf16 tensor [rows][cols] (row stride ld elements), box = kBK cols x box_rows rows, 128B swizzle.
+int make_map(CUtensorMap* out, const void* ptr, long long rows, long long cols, long long ld, int box_rows) {
+  static std::mutex mu;
+  static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+  MapKey key{ptr, rows, cols, ld, box_rows};
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *out = it->second;
+      return 0;
+    }
+  }
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return ASTRAEA_EUNSUPPORTED;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return ASTRAEA_EINVAL;
+  std::lock_guard<std::mutex> g(mu);
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(key, *out);
+  return 0;
+}
+
+}  // namespace tc
+}  // namespace astraea
 
 static unsigned long long* g_trace = nullptr;
 static int g_trace_slots = 0, g_trace_next = 0, g_trace_stride = 0;

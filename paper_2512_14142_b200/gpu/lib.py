@@ -15,7 +15,7 @@ from pathlib import Path
 
 from ..host.errors import DeviceError
 
-LIB_PATH = Path(__file__).resolve().parent.parent / "lib" / "libastraea_b200.so"
+LIB_PATH = Path(os.environ.get("ASTRAEA_LIB", Path(__file__).resolve().parent.parent / "lib" / "libastraea_b200.so"))
 
 SWAP_KERNEL = 0
 SWAP_DMA = 1
@@ -75,6 +75,31 @@ class GemmPhase(ctypes.Structure):
 EPI_SILU = 2
 EPI_QKV_ROPE = 3
 EPI_ARGMAX = 4
+PHASE_GEMM = 0
+PHASE_ATTN = 1
+
+
+class StepPhase(ctypes.Structure):
+    """astraea_step_phase (include/astraea_b200.h)."""
+
+    _fields_ = [
+        ("kind", ctypes.c_int32),
+        ("gemm", GemmPhase),
+        ("a_from", ctypes.c_int32),
+        ("epi_from", ctypes.c_int32),
+        ("pool_dev", ctypes.c_void_p),
+        ("geo", KvGeometry),
+        ("layer", ctypes.c_int32),
+        ("num_q_heads", ctypes.c_int32),
+        ("q_dev", ctypes.c_void_p),
+        ("q_row_stride", ctypes.c_int32),
+        ("table_dev", ctypes.c_void_p),
+        ("max_blocks", ctypes.c_int32),
+        ("ctx_dev", ctypes.c_void_p),
+        ("scale", ctypes.c_float),
+        ("out_dev", ctypes.c_void_p),
+        ("qkv_from", ctypes.c_int32),
+    ]
 
 _i32 = ctypes.c_int32
 _vp = ctypes.c_void_p
@@ -113,6 +138,11 @@ SIGNATURES = {
     "astraea_rope_table": (ctypes.c_int, [_vp, _i32, _i32, _f32, _vp, _vp]),
     "astraea_gemm_chain_workspace_bytes": (_sz, [_i32, _i32, ctypes.POINTER(GemmPhase)]),
     "astraea_gemm_chain": (ctypes.c_int, [_i32, _i32, ctypes.POINTER(GemmPhase), _vp, _sz, _vp]),
+    "astraea_step_program_bytes": (_sz, [_i32]),
+    "astraea_step_workspace_bytes": (_sz, [_i32, _i32, ctypes.POINTER(StepPhase)]),
+    "astraea_step_program_build": (ctypes.c_int, [_i32, _i32, ctypes.POINTER(StepPhase), _vp, _sz, _vp, _sz]),
+    "astraea_step_launch": (ctypes.c_int, [_i32, _i32, _vp, _vp, _i32, _vp]),
+    "astraea_debug_step_trace": (ctypes.c_int, [_vp]),
     "astraea_decode_advance": (
         ctypes.c_int, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp]),
     "astraea_rmsnorm": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _f32, _vp]),

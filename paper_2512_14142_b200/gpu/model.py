@@ -184,6 +184,15 @@ class LlamaRunner:
         self.device = dev
         self.parts = -(-d // 128)
         self.use_chain = True   # decode GEMMs as one persistent chain per layer (False: one launch each)
+        # decode step as ONE persistent kernel (astraea_step_launch). Off by
+        # default: on B200 it matches the per-layer chain at batch 1 and trails
+        # it at larger batches ("decode-step kernel")
+        self.use_step_kernel = False
+        self.l2_ahead = 0
+        self._mk = None
+        self._programs: dict = {}
+        self.last_program = None
+        self.step_ws = ops.StepWorkspace()
 
     def _dec_ws(self, B, max_blocks):
         need = L.load().astraea_decode_workspace_bytes(B, self.cfg.num_q_heads, self.cfg.head_dim, max_blocks)
@@ -270,7 +279,13 @@ class LlamaRunner:
         the paged attention and ONE chained GEMM kernel running O-proj ->
         gate/up -> down -> next layer's QKV (the last layer's chain ends
         with lm_head + argmax instead) -- 2 launches per layer."""
-        if want_logits or not self.use_chain or self.cfg.num_layers < 1 or tokens.shape[0] > 64:
+        if self.cfg.num_layers < 1 or tokens.shape[0] > 64:
+            return self._decode_unchained(tokens, positions, slots, table, ctx, stream, want_logits, keys_out)
+        if self.use_step_kernel and self._step_supported():
+            return self._decode_step_kernel(tokens, positions, slots, table, ctx, stream, keys_out, want_logits)
+        if want_logits:
+            return self._decode_unchained(tokens, positions, slots, table, ctx, stream, want_logits, keys_out)
+        if not self.use_chain:
             return self._decode_unchained(tokens, positions, slots, table, ctx, stream, want_logits, keys_out)
         cfg, w, pool = self.cfg, self.w, self.pool
         B = tokens.shape[0]
@@ -308,6 +323,107 @@ class LlamaRunner:
                 phases.append(dict(a=x, w=w.lm_head, out=None, kind=L.EPI_ARGMAX, ssq_in=ssq, rms_dim=d, rms_eps=eps,
                                    argmax_keys=keys))
             ops.gemm_chain(phases, ws, stream=stream)
+        if keys_out is not None:
+            return keys_out
+        return ops.keys_to_ids(keys)
+
+    def _step_supported(self) -> bool:
+        cfg = self.cfg
+        G = cfg.num_q_heads // cfg.num_kv_heads
+        return (cfg.head_dim, G) in ((128, 4), (64, 2), (64, 4))
+
+    def _mk_bufs(self):
+        """Persistent activation buffers of the step kernel (max_rows rows):
+        the program's TMA descriptors point at them, so they never move."""
+        if self._mk is None:
+            cfg, R, dev = self.cfg, self.max_rows, self.device
+            qd = cfg.num_q_heads * cfg.head_dim
+            bf = dict(dtype=torch.bfloat16, device=dev)
+            self._mk = {
+                "x": torch.zeros(R, cfg.hidden, **bf), "q": torch.zeros(R, qd, **bf),
+                "att": torch.zeros(R, qd, **bf), "h": torch.zeros(R, cfg.ffn, **bf),
+                "ssq0": torch.zeros(1, R, dtype=torch.float32, device=dev),
+                "ssq_mid": torch.zeros(self.parts, R, dtype=torch.float32, device=dev),
+                "ssq": torch.zeros(self.parts, R, dtype=torch.float32, device=dev),
+                "cs": torch.zeros(R, cfg.head_dim // 2, 2, dtype=torch.float32, device=dev),
+            }
+        return self._mk
+
+    def step_phases(self, B, positions, slots, table, ctx, keys, logits=None):
+        """The decode step as a phase program (see ops.StepProgram): per layer
+        QKV(+RoPE+append) -> ATTN -> O(+residual) -> gate/up(+SiLU) ->
+        down(+residual), the last layer's down feeding lm_head + argmax."""
+        cfg, w, pool = self.cfg, self.w, self.pool
+        mb = self._mk_bufs()
+        x, q, att, h = mb["x"][:B], mb["q"][:B], mb["att"][:B], mb["h"][:B]
+        P = self.parts
+        ssq0 = mb["ssq0"].view(-1)[:B].view(1, B)
+        ssq_mid = mb["ssq_mid"].view(-1)[:P * B].view(P, B)
+        ssq = mb["ssq"].view(-1)[:P * B].view(P, B)
+        cs = mb["cs"][:B]
+        d, eps, qd = cfg.hidden, cfg.eps, cfg.num_q_heads * cfg.head_dim
+        phases = []
+
+        def qkv(li, ssq_in, a_from):
+            phases.append(dict(kind="gemm", a=x, w=w.layers[li]["wqkv"], out=q, epi=L.EPI_QKV_ROPE, a_from=a_from,
+                               epi_from=a_from, ssq_in=ssq_in, rms_dim=d,
+                               rms_eps=eps, pool=pool.data, geo=pool.geo, layer=li, num_q_heads=cfg.num_q_heads,
+                               positions=positions, slots=slots, rope_theta=cfg.rope_theta, rope_table=cs))
+            return len(phases) - 1
+
+        i_qkv = qkv(0, ssq0, -1)
+        i_down = -1
+        for li, lw in enumerate(w.layers):
+            phases.append(dict(kind="attn", pool=pool.data, geo=pool.geo, layer=li, num_q_heads=cfg.num_q_heads,
+                               q=q, q_stride=qd, table=table, ctx=ctx, scale=self.scale, out=att, qkv_from=i_qkv))
+            i_att = len(phases) - 1
+            phases.append(dict(kind="gemm", a=att, w=lw["wo"], out=x, epi=L.EPI_RESIDUAL, residual=x,
+                               ssq_out=ssq_mid, a_from=i_att, epi_from=i_down))
+            i_o = len(phases) - 1
+            phases.append(dict(kind="gemm", a=x, w=lw["wgu"], out=h, epi=L.EPI_SILU, ssq_in=ssq_mid, rms_dim=d,
+                               rms_eps=eps, a_from=i_o, epi_from=i_o))
+            i_gu = len(phases) - 1
+            phases.append(dict(kind="gemm", a=h, w=lw["wdown"], out=x, epi=L.EPI_RESIDUAL, residual=x,
+                               ssq_out=ssq, a_from=i_gu, epi_from=i_o))
+            i_down = len(phases) - 1
+            if li + 1 < cfg.num_layers:
+                i_qkv = qkv(li + 1, ssq, i_down)
+        phases.append(dict(kind="gemm", a=x, w=w.lm_head, out=logits, epi=L.EPI_ARGMAX, ssq_in=ssq, rms_dim=d,
+                           rms_eps=eps, argmax_keys=keys, a_from=i_down, epi_from=i_down))
+        return phases
+
+    def _decode_step_kernel(self, tokens, positions, slots, table, ctx, stream=None, keys_out=None,
+                            want_logits=False):
+        """Embedding + RoPE table + ONE persistent launch for every layer and
+        the sampling (astraea_step_launch)."""
+        cfg = self.cfg
+        B = tokens.shape[0]
+        dev = tokens.device
+        mb = self._mk_bufs()
+        keys = keys_out if keys_out is not None else torch.zeros(B, dtype=torch.int64, device=dev)
+        ops.embedding(tokens, self.w.embed, out=mb["x"][:B], ssq_out=mb["ssq0"].view(-1)[:B], stream=stream)
+        ops.rope_table(positions, cfg.head_dim, cfg.rope_theta, out=mb["cs"][:B], stream=stream)
+        logits = None
+        if want_logits:
+            if "logits" not in mb:
+                mb["logits"] = torch.zeros(self.max_rows, cfg.vocab, dtype=torch.bfloat16, device=dev)
+            logits = mb["logits"][:B]
+        key = (B, positions.data_ptr(), slots.data_ptr(), table.data_ptr(), table.shape[1], ctx.data_ptr(),
+               keys.data_ptr(), want_logits)
+        prog = self._programs.get(key)
+        if prog is None:
+            s = stream if stream is not None else torch.cuda.current_stream()
+            with torch.cuda.stream(s):
+                prog = ops.StepProgram(B, self.step_phases(B, positions, slots, table, ctx, keys, logits),
+                                       self.step_ws)
+            if len(self._programs) >= 16:
+                self._programs.pop(next(iter(self._programs)))
+            self._programs[key] = prog
+        self.last_program = prog
+        prog.launch(stream, self.l2_ahead)
+        if want_logits:
+            ids = ops.keys_to_ids(keys)
+            return ids, logits.clone()
         if keys_out is not None:
             return keys_out
         return ops.keys_to_ids(keys)

@@ -104,6 +104,81 @@ def gemm_chain(phases, workspace, stream=None):
     _count()
 
 
+class StepProgram:
+    """A decode step as one persistent launch (astraea_step_program_build /
+    astraea_step_launch).
+
+    ``phases``: dicts in program order. GEMM phases: ``kind="gemm"``, ``a``,
+    ``w``, ``out``, ``epi`` (the epilogue kind) and the other ``gemm_ex``
+    epilogue keywords, plus ``a_from`` /
+    ``epi_from`` (indices of the producing phases, -1 for launch inputs).
+    ATTN phases: ``kind="attn"``, ``pool``, ``geo``, ``layer``,
+    ``num_q_heads``, ``q``, ``q_stride``, ``table``, ``ctx``, ``scale``,
+    ``out``, ``qkv_from``. All rows: M <= 64. The tensors must stay alive
+    (and at the same addresses) for as long as the program is launched.
+    """
+
+    def __init__(self, M, phases, workspace_pool):
+        lib = L.require_cuda()
+        n = len(phases)
+        arr = (L.StepPhase * n)()
+        for i, ph in enumerate(phases):
+            q = arr[i]
+            q.a_from = ph.get("a_from", -1)
+            q.epi_from = ph.get("epi_from", -1)
+            q.qkv_from = ph.get("qkv_from", -1)
+            if ph["kind"] == "gemm":
+                q.kind = L.PHASE_GEMM
+                a, w, out = ph["a"], ph["w"], ph.get("out")
+                g = q.gemm
+                g.A, g.lda = L.ptr(a), a.stride(0)
+                g.W, g.ldw = L.ptr(w), w.stride(0)
+                g.C, g.ldc = L.ptr(out), (out.stride(0) if out is not None else 0)
+                g.N, g.K = w.shape[0], a.shape[1]
+                g.epi = _epilogue(kind=ph.get("epi", L.EPI_NONE),
+                                  **{k: v for k, v in ph.items()
+                                     if k not in ("kind", "epi", "a", "w", "out", "a_from", "epi_from", "qkv_from")})
+            else:
+                q.kind = L.PHASE_ATTN
+                q.pool_dev, q.geo, q.layer = L.ptr(ph["pool"]), ph["geo"], ph["layer"]
+                q.num_q_heads, q.q_dev, q.q_row_stride = ph["num_q_heads"], L.ptr(ph["q"]), ph["q_stride"]
+                q.table_dev, q.max_blocks = L.ptr(ph["table"]), ph["table"].shape[1]
+                q.ctx_dev, q.scale, q.out_dev = L.ptr(ph["ctx"]), ph["scale"], L.ptr(ph["out"])
+        self.M, self.n = M, n
+        dev = phases[0].get("a", phases[0].get("q")).device
+        need = lib.astraea_step_workspace_bytes(M, n, arr)
+        if need == 0:
+            raise L.DeviceError("decode step program rejected (shapes)")
+        self.ws = workspace_pool.get(need, dev)
+        nb = lib.astraea_step_program_bytes(n)
+        self.host = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
+        L.check(lib.astraea_step_program_build(M, n, arr, L.ptr(self.host), nb, L.ptr(self.ws),
+                                               self.ws.numel() * 4), "step_program_build")
+        self.prog = torch.empty(nb, dtype=torch.uint8, device=dev)
+        self.prog.copy_(self.host, non_blocking=True)   # stream-ordered before the first launch
+        self.keep = phases   # tensors referenced by the program
+
+    def launch(self, stream=None, l2_ahead=0):
+        lib = L.require_cuda()
+        L.check(lib.astraea_step_launch(self.M, self.n, L.ptr(self.prog), L.ptr(self.ws), l2_ahead, _s(stream)),
+                "step_launch")
+        _count()
+
+
+class StepWorkspace:
+    """Zero-filled step workspace shared by the programs of one stream (it
+    holds the launch epoch and the dataflow flags). Grows by replacement;
+    programs built on an older buffer keep it alive."""
+
+    def __init__(self):
+        self.buf = None
+
+    def get(self, nbytes, device):
+        if self.buf is None or self.buf.numel() * 4 < nbytes:
+            self.buf = torch.zeros(nbytes // 4 + 64, dtype=torch.float32, device=device)
+        return self.buf
+
+
 def gemm_ex(a, w, out, kind=L.EPI_NONE, residual=None, ssq_out=None, ssq_in=None, rms_dim=0, rms_eps=1e-5,
             pool=None, geo=None, layer=0, num_q_heads=0, positions=None, slots=None, rope_theta=0.0,
             rope_table=None, argmax_keys=None, workspace=None, stream=None):

@@ -133,6 +133,7 @@ def test_chained_decode_step_equals_unchained(B):
     for chained in (True, False):
         pool = KvPool(cfg, 64)
         runner = LlamaRunner(w, pool)
+        runner.use_step_kernel = False
         for b in range(B):
             ids = segment_token_ids(f"c{b}", 1, 20 + b, cfg.vocab)
             _prefill_one(runner, pool, ids, [4 * b, 4 * b + 1, 4 * b + 2, 4 * b + 3])
