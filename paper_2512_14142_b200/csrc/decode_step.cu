@@ -125,14 +125,6 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
   asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 __device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ bool flag_set(const int* flags, int i, int epoch) {
   return ld_relaxed(flags + i * kFlagStride) == epoch;
@@ -848,7 +840,7 @@ __global__ void __launch_bounds__(kMkThreads, 1)
             // Partials are self-validating 64-bit words (fp32 bits | tag << 32,
             // single-copy atomic): each thread spins on its own values, so
             // waiting and loading are one round trip and need no flag.
-            constexpr int GRP = BN == 16 ? 4 : (BN == 32 ? 2 : 1);
+            constexpr int GRP = 1;
             for (int c0 = c_first + 1; c0 <= c_last; c0 += GRP) {
               unsigned long long pv[GRP][BN];
 #pragma unroll

@@ -43,6 +43,7 @@
 #include "common.cuh"
 #include "tc.cuh"
 
+
 using namespace astraea;
 using namespace astraea::tc;
 
@@ -372,7 +373,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
   bf16* xch = reinterpret_cast<bf16*>(tmem_slot + 4);        // [BN][128]
   float* red = reinterpret_cast<float*>(xch + BN * kBM);     // [4][BN]
   float* rs = red + 4 * BN;                                  // [BN]
-  __shared__ int s_last;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
@@ -481,6 +481,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     if (tr && lane == 0) tr[9] = gtimer();
   } else {
     pdl_wait();
+    const int epoch = __ldcg(args.phase_ctr + kMaxPhases + 1) + 1;   // launches completed on this workspace + 1
     const int quarter = warp & 3;
     const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
     const int row = quarter * 32 + lane;  // feature within the tile
@@ -502,12 +503,64 @@ __global__ void __launch_bounds__(kThreads, MINB)
         if (row < args.M) rs[row] = rms_scale(P.epi, args.M, row);
         epi_bar();
       }
+      // Split tiles are finished by c_first, the CTA owning the tile's first
+      // k-blocks: its segment closes its range while the others open theirs,
+      // so their partials are normally in L2 long before. Partials are
+      // self-validating 64-bit words (fp32 bits | tag << 32, single-copy
+      // atomic): the finisher loads them while its own last MMAs run and
+      // spins only on words not yet written -- no arrival counter and no
+      // round trip after the last MMA. Sum order: the other segments in CTA
+      // order, then the finisher's own (deterministic).
+      const unsigned tag = ((unsigned)epoch << 3) | (unsigned)p;
+      const bool resid = P.epi.kind == EPI_RESIDUAL;
+      unsigned long long* wsq = reinterpret_cast<unsigned long long*>(args.ws);
       for (long long u = u0; u < u1; ++seg) {
         const long long tile = u / KB;
         const long long seg_end = min(u1, (tile + 1) * KB);
         const bool whole = (u == tile * KB) && (seg_end == (tile + 1) * KB);
         u = seg_end;
         const int buf = seg & 1;
+        const long long first_u = tile * KB;
+        const int c_first = whole ? cta : sk_owner(first_u, U, P.geff);
+        const int c_last = whole ? cta : sk_owner(first_u + KB - 1, U, P.geff);
+        const bool finisher = cta == c_first;
+        unsigned long long* tpart = wsq + ((tile * P.maxseg) * (long long)args.M) * kBM + row;
+        constexpr bool kPreRes = BN <= 32;   // register budget: BN = 64 reads the residual in the epilogue
+        float res[BN], acc[BN];
+        if (finisher) {
+          if (kPreRes && resid) {
+            const int f = (int)tile * kBM + row;
+#pragma unroll
+            for (int t = 0; t < BN; ++t)
+              res[t] = (t < args.M && f < P.N) ? bf2f(__ldcg(P.epi.residual + (long long)t * P.ldc + f)) : 0.f;
+          }
+#pragma unroll
+          for (int t = 0; t < BN; ++t) acc[t] = 0.f;
+          constexpr int GRP = 1;   // one segment's words in flight at a time (register budget; measured best)
+          for (int c0 = c_first + 1; c0 <= c_last; c0 += GRP) {
+            unsigned long long pv[GRP][BN];
+#pragma unroll
+            for (int k = 0; k < GRP; ++k) {
+              const unsigned long long* pp = tpart + (long long)(c0 + k - c_first) * args.M * kBM;
+#pragma unroll
+              for (int t = 0; t < BN; ++t)
+                pv[k][t] = (c0 + k <= c_last && t < args.M) ? ld_relaxed_u64(pp + (long long)t * kBM) : 0ull;
+            }
+#pragma unroll
+            for (int k = 0; k < GRP; ++k) {
+              if (c0 + k <= c_last) {
+                const unsigned long long* pp = tpart + (long long)(c0 + k - c_first) * args.M * kBM;
+#pragma unroll
+                for (int t = 0; t < BN; ++t) {
+                  if (t < args.M) {
+                    while ((unsigned)(pv[k][t] >> 32) != tag) pv[k][t] = ld_relaxed_u64(pp + (long long)t * kBM);
+                    acc[t] += __uint_as_float((unsigned)pv[k][t]);
+                  }
+                }
+              }
+            }
+          }
+        }
         mbar_wait(&tfull[buf], (seg >> 1) & 1);
         tc_fence_after();
         float v[BN < 32 ? 32 : BN];
@@ -516,63 +569,20 @@ __global__ void __launch_bounds__(kThreads, MINB)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
-        if (whole) {
-          sk_finish<BN>(P, (int)tile, row, v, rs, xch, red);
+        if (!finisher) {
+          unsigned long long* pp = tpart + (long long)(cta - c_first) * args.M * kBM;
+#pragma unroll
+          for (int t = 0; t < BN; ++t)
+            if (t < args.M)
+              st_relaxed_u64(pp + (long long)t * kBM,
+                             (unsigned long long)__float_as_uint(v[t]) | ((unsigned long long)tag << 32));
           continue;
         }
-        const long long first_u = tile * KB;
-        const int c_first = sk_owner(first_u, U, P.geff);
-        const int nseg = sk_owner(first_u + KB - 1, U, P.geff) - c_first + 1;
-        const int sidx = cta - c_first;
-        float* part = args.ws + ((tile * P.maxseg + sidx) * (long long)args.M) * kBM;
+        if (!whole) {
 #pragma unroll
-        for (int t = 0; t < BN; ++t)
-          if (t < args.M) __stcg(part + (long long)t * kBM + row, v[t]);
-        // One release/acquire RMW per CTA after the barrier publishes the
-        // whole CTA's partial (cumulativity through bar.sync).
-        epi_bar();
-        if (threadIdx.x == 64) s_last = atom_add_acq_rel(args.counters + tile, 1) == nseg - 1;
-        epi_bar();
-        if (s_last) {
-          const float* base = args.ws + (tile * P.maxseg * (long long)args.M) * kBM + row;
-          // Partials are added in segment order (deterministic). For BN <= 32
-          // two segments' loads are in flight together and this CTA's own
-          // partial comes from registers; BN = 64 reloads it (register budget).
-          if constexpr (BN <= 32) {
-            float own[BN];
-#pragma unroll
-            for (int t = 0; t < BN; ++t) {
-              own[t] = v[t];
-              v[t] = 0.f;
-            }
-            for (int sg = 0; sg < nseg; sg += 2) {
-              float p0[BN], p1[BN];
-#pragma unroll
-              for (int t = 0; t < BN; ++t) {
-                p0[t] = (t < args.M && sg != sidx) ? __ldcg(base + ((long long)sg * args.M + t) * kBM) : own[t];
-                p1[t] = (t < args.M && sg + 1 < nseg && sg + 1 != sidx)
-                            ? __ldcg(base + ((long long)(sg + 1) * args.M + t) * kBM) : own[t];
-              }
-#pragma unroll
-              for (int t = 0; t < BN; ++t) {
-                v[t] += p0[t];
-                if (sg + 1 < nseg) v[t] += p1[t];
-              }
-            }
-          } else {
-#pragma unroll
-            for (int t = 0; t < BN; ++t) v[t] = 0.f;
-            for (int sg = 0; sg < nseg; ++sg) {
-              float p0[BN];
-#pragma unroll
-              for (int t = 0; t < BN; ++t) p0[t] = t < args.M ? __ldcg(base + ((long long)sg * args.M + t) * kBM) : 0.f;
-#pragma unroll
-              for (int t = 0; t < BN; ++t) v[t] += p0[t];
-            }
-          }
-          if (threadIdx.x == 64) args.counters[tile] = 0;
-          sk_finish<BN>(P, (int)tile, row, v, rs, xch, red);
+          for (int t = 0; t < BN; ++t) v[t] = acc[t] + v[t];
         }
+        sk_finish<BN>(P, (int)tile, row, v, rs, xch, red, (kPreRes && resid) ? res : nullptr);
       }
       // phase p done in this CTA: publish (release) for the other CTAs
       epi_bar();
@@ -589,6 +599,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     // the last CTA to leave resets the phase counters for the next launch
     if (atom_add_acq_rel(args.phase_ctr + kMaxPhases, 1) == G - 1) {
       for (int p = 0; p <= kMaxPhases; ++p) args.phase_ctr[p] = 0;
+      args.phase_ctr[kMaxPhases + 1] += 1;   // launch epoch (tags of the stream-K partials)
     }
     if (tr) tr[10] = gtimer();
   }
@@ -646,7 +657,7 @@ SkPlan sk_plan(int M, int N, int K) {
 constexpr size_t kCounterBytes = 16384 * sizeof(int);
 constexpr size_t kPhaseBytes = 256;
 
-size_t partial_bytes(int M, const SkPlan& p) { return (size_t)p.tiles * p.maxseg * M * kBM * sizeof(float); }
+size_t partial_bytes(int M, const SkPlan& p) { return (size_t)p.tiles * p.maxseg * M * kBM * sizeof(unsigned long long); }
 
 template <int BN>
 constexpr size_t sk_extra_bytes() {

@@ -187,6 +187,15 @@ __device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
   return prev;
 }
 
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 // Finish one 128-feature tile: thread `row` holds v[t] (t < M) of feature
 // tile*128 + row. All 128 epilogue threads call this together.
 template <int BN, typename A>
