@@ -20,6 +20,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "attn_mma.cuh"
 
 using namespace astraea;
 
@@ -308,6 +309,139 @@ __global__ void __launch_bounds__(128) decode_kernel(const __grid_constant__ Dec
   }
 }
 
+// Tensor-core decode attention: one CTA per (context split, kv head, row),
+// four warps taking every fourth page of the split (attn_mma.cuh: mma.sync
+// scores and PV with the G q heads as the M rows), merged in shared memory;
+// splits are merged (log-sum-exp, split order) by the last split CTA. Only
+// ~17 KB of shared memory, so the next layer's GEMM CTAs (PDL) are resident
+// beside it and stream their first weight tiles during the attention.
+template <int D, int G>
+constexpr int decode_mma_warp_bytes() {   // a V page, or the warp's merged state ([G] m, [G] l, [G][D] o)
+  return kBT * D * 2 > (2 * G + G * D) * 4 ? kBT * D * 2 : (2 * G + G * D) * 4;
+}
+
+template <int D, int G>
+__global__ void __launch_bounds__(128) decode_mma_kernel(const __grid_constant__ DecodeParams p) {
+  using namespace astraea::attn;
+  constexpr int EPT = (G * D + 127) / 128;
+  constexpr int WREG = decode_mma_warp_bytes<D, G>() / 2;   // per-warp region (bf16 elements)
+  extern __shared__ __align__(128) uint8_t dsm[];
+  bf16* vs_all = reinterpret_cast<bf16*>(dsm);   // [4][WREG]: V page, then the warp's state
+  const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  pdl_wait();
+  pdl_launch();
+  const int ctx = p.ctx[b];
+  const int nblk = (ctx + kBT - 1) / kBT;
+  const int b0 = split * p.blocks_per_split;
+  const int b1 = min(nblk, b0 + p.blocks_per_split);
+  const int r8 = lane >> 2, quad = lane & 3;
+  uint32_t qa[D / 8];
+  attn_load_q<D>(p.q + (long long)b * p.q_stride + (long long)(h * G + r8) * D, r8 < G, quad, qa);
+  const PageSrc src = page_src<D>(p.pool, p.block_el, p.layer, p.Hkv, h, p.table + (long long)b * p.max_blocks,
+                                  p.scale_log2);
+  bf16* vs = vs_all + warp * WREG;
+  AttnAcc<D> st;
+  attn_pages<D>(src, b0 + warp, b1, 4, ctx, qa, vs, st, lane);
+  // merge the 4 warps (warp order) through shared memory
+  float* wst = reinterpret_cast<float*>(vs);   // [G] m, [G] l, [G][D] o (the warp's V page is free now)
+  __syncwarp();
+  if (r8 < G) {
+#pragma unroll
+    for (int n = 0; n < D / 8; ++n)
+      *reinterpret_cast<float2*>(wst + 2 * G + r8 * D + 8 * n + 2 * quad) = make_float2(st.o[n][0], st.o[n][1]);
+    if (quad == 0) {
+      wst[r8] = st.m;
+      wst[G + r8] = st.l;
+    }
+  }
+  __syncthreads();
+  float Mv[EPT], Lv[EPT], Ov[EPT];
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int idx = tid * EPT + e, g = idx / D, dd = idx % D;
+    Mv[e] = -INFINITY;
+    Lv[e] = 0.f;
+    Ov[e] = 0.f;
+    if (idx < G * D) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const float* ws = reinterpret_cast<const float*>(vs_all + w * WREG);
+        const float mk = ws[g], mn = fmaxf(Mv[e], mk);
+        const float a0 = mn == -INFINITY ? 0.f : exp2f(Mv[e] - mn), a1 = mn == -INFINITY ? 0.f : exp2f(mk - mn);
+        Lv[e] = Lv[e] * a0 + ws[G + g] * a1;
+        Ov[e] = Ov[e] * a0 + ws[2 * G + g * D + dd] * a1;
+        Mv[e] = mn;
+      }
+    }
+  }
+  if (p.splits == 1) {
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int idx = tid * EPT + e, g = idx / D, dd = idx % D;
+      if (idx < G * D) p.out[((long long)b * p.Hq + h * G + g) * D + dd] = f2bf(Lv[e] > 0.f ? Ov[e] / Lv[e] : 0.f);
+    }
+    return;
+  }
+  // split partial: normalised o and log-sum-exp per q head
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int idx = tid * EPT + e, g = idx / D, dd = idx % D;
+    if (idx < G * D) {
+      const long long row = ((long long)b * p.Hq + h * G + g) * p.splits + split;
+      __stcg(p.ws_o + row * D + dd, Lv[e] > 0.f ? Ov[e] / Lv[e] : 0.f);
+      if (dd == 0) __stcg(p.ws_lse + row, Lv[e] > 0.f ? Mv[e] + log2f(Lv[e]) : -INFINITY);
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ int s_last;
+  int* ctr = p.counters + (long long)b * p.Hkv + h;
+  if (tid == 0) s_last = atomicAdd(ctr, 1) == p.splits - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  __shared__ float wsh[G][kMaxSplits];
+  __shared__ float den_sh[G];
+  const long long bh0 = (long long)b * p.Hq + h * G;
+  for (int i = tid; i < G * p.splits; i += 128) {
+    const int g = i / p.splits, sp = i % p.splits;
+    wsh[g][sp] = __ldcg(p.ws_lse + (bh0 + g) * p.splits + sp);
+  }
+  __syncthreads();
+  if (tid < G) {
+    float mx = -INFINITY;
+    for (int sp = 0; sp < p.splits; ++sp) mx = fmaxf(mx, wsh[tid][sp]);
+    float den = 0.f;
+    for (int sp = 0; sp < p.splits; ++sp) {
+      const float w = (mx == -INFINITY || wsh[tid][sp] == -INFINITY) ? 0.f : exp2f(wsh[tid][sp] - mx);
+      wsh[tid][sp] = w;
+      den += w;
+    }
+    den_sh[tid] = den;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int idx = tid * EPT + e, g = idx / D, dd = idx % D;
+    if (idx >= G * D) continue;
+    const long long row0 = (bh0 + g) * p.splits;
+    float num = 0.f;
+    int sp = 0;
+    for (; sp + 4 <= p.splits; sp += 4) {
+      float o4[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o4[k] = __ldcg(p.ws_o + (row0 + sp + k) * D + dd);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) num += wsh[g][sp + k] * o4[k];
+    }
+    for (; sp < p.splits; ++sp) num += wsh[g][sp] * __ldcg(p.ws_o + (row0 + sp) * D + dd);
+    const float den = den_sh[g];
+    p.out[(bh0 + g) * D + dd] = f2bf(den > 0.f ? num / den : 0.f);
+  }
+  if (tid == 0) *ctr = 0;
+}
+
 // ---------------------------------------------------------------------------
 // K7 prefill (mma.sync m16n8k16, bf16 in, fp32 accumulate)
 // ---------------------------------------------------------------------------
@@ -534,7 +668,10 @@ __global__ void __launch_bounds__(128) prefill_kernel(const __grid_constant__ Pr
 int decode_splits(int B, int Hkv, int max_blocks, int* bps) {
   // Enough CTAs to cover the SMs, but at least kMinBlocks blocks (8 KiB of
   // K+V per head per block) per CTA so per-CTA fixed costs stay small.
-  constexpr int kMinBlocks = 8;
+  static const int kMinBlocks = [] {
+    const char* e = getenv("ASTRAEA_DECODE_MIN_BLOCKS");
+    return e ? std::max(1, atoi(e)) : 8;
+  }();
   const int target = 2 * num_sms();
   const int base = B * Hkv;
   int want = (target + base - 1) / base;
@@ -609,7 +746,20 @@ extern "C" int astraea_paged_decode_attention(const astraea_kv_geometry* g, cons
     }                                                                                                \
     ASTRAEA_TRY(launch_k(decode_kernel<DD, GG>, grid, dim3(128), smem, st, p));                     \
   } while (0)
-  if (D == 128 && G == 4) LAUNCH_DEC(128, 4);
+#define LAUNCH_MMA(DD, GG)                                                                         \
+  do {                                                                                               \
+    constexpr size_t smem = 4 * decode_mma_warp_bytes<DD, GG>();                                   \
+    ASTRAEA_TRY(launch_k(decode_mma_kernel<DD, GG>, grid, dim3(128), smem, st, p));                 \
+  } while (0)
+  static const bool use_mma = [] {
+    const char* e = getenv("ASTRAEA_DECODE_ATTN");
+    return !(e && e[0] == 's');   // "simt": the CUDA-core kernel
+  }();
+  if (use_mma && D == 128 && G == 4) LAUNCH_MMA(128, 4);
+  else if (use_mma && D == 128 && G == 8) LAUNCH_MMA(128, 8);
+  else if (use_mma && D == 64 && G == 4) LAUNCH_MMA(64, 4);
+  else if (use_mma && D == 64 && G == 2) LAUNCH_MMA(64, 2);
+  else if (D == 128 && G == 4) LAUNCH_DEC(128, 4);
   else if (D == 128 && G == 8) LAUNCH_DEC(128, 8);
   else if (D == 64 && G == 4) LAUNCH_DEC(64, 4);
   else if (D == 64 && G == 8) LAUNCH_DEC(64, 8);
@@ -618,6 +768,7 @@ extern "C" int astraea_paged_decode_attention(const astraea_kv_geometry* g, cons
   else if (D == 128 && G == 1) LAUNCH_DEC(128, 1);
   else return ASTRAEA_EUNSUPPORTED;
 #undef LAUNCH_DEC
+#undef LAUNCH_MMA
   ASTRAEA_CHECK_LAUNCH();
   return ASTRAEA_OK;
 }
