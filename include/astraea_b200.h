@@ -233,6 +233,7 @@ typedef struct {
   float rope_theta;
   const float* rope_table_dev; /* optional [M][head_dim/2] (cos, sin) pairs from astraea_rope_table */
   unsigned long long* argmax_keys_dev; /* ARGMAX: [M] */
+  int32_t argmax_col_offset;           /* ARGMAX: added to the column index in the key (vocab-sharded lm_head) */
 } astraea_epilogue;
 /* A chain of dependent decode GEMMs (M <= 64 tokens) in ONE persistent launch
  * (e.g. O-proj -> gate/up -> down -> next layer's QKV, or ... -> lm_head +
@@ -324,6 +325,12 @@ ASTRAEA_API int astraea_debug_gemm_trace(void* buf, int32_t slots, int32_t slot_
  * i < D/2 -- computed once per forward and shared by every layer's QKV epilogue. */
 ASTRAEA_API int astraea_rope_table(const int32_t* positions_dev, int32_t T, int32_t head_dim, float rope_theta,
                        float* table_dev, void* stream);
+
+/* Per-row sums of squares in 128-column groups: ssq_out[ceil(dim/128)][rows]
+ * (the layout the GEMM epilogues' ssq_in reads) -- the RMSNorm statistics of
+ * a hidden state produced outside a fused epilogue (e.g. after a
+ * tensor-parallel all-reduce). */
+ASTRAEA_API int astraea_row_ssq(const void* x_dev, int32_t rows, int32_t dim, float* ssq_out_dev, void* stream);
 
 /* ---- K8: small fused ops --------------------------------------------------------------------------- */
 /* y = rmsnorm(x + r) * w ; if resid_out_dev != NULL it receives x + r. r may be NULL. */

@@ -75,3 +75,44 @@ def greedy_continue(w, cfg, ids, n_steps, bf16_points=True):
         out.append(nxt)
         seq.append(nxt)
     return out
+
+
+def forward_tp(w, cfg, ids, rank, world, all_reduce, all_gather, bf16_points=True):
+    """Tensor-parallel restatement (paper_2512_14142_b200.gpu.tp): `w` is this
+    rank's shard (tp.shard_logical) of a model with full config `cfg`. The O
+    and down projections produce partial sums (rank 0 adds the residual) that
+    are all-reduced; the lm_head logits slices are all-gathered. Returns the
+    full logits [T, vocab] on every rank."""
+    T = len(ids)
+    Hq, Hkv, D = cfg.num_q_heads // world, cfg.num_kv_heads // world, cfg.head_dim
+    G = Hq // Hkv
+    r = lambda t: _r(t, bf16_points)  # noqa: E731
+    pos = torch.arange(T)
+    x = w["embed"][torch.as_tensor(ids, dtype=torch.long)].float()
+    mask = torch.triu(torch.ones(T, T, dtype=torch.bool), 1)
+    for lw in w["layers"]:
+        h = rmsnorm(x, lw["attn_norm"].float(), cfg.eps)
+        qkv = r(h @ lw["wqkv"].float().T)
+        q = qkv[:, : Hq * D].view(T, Hq, D)
+        k = qkv[:, Hq * D: (Hq + Hkv) * D].view(T, Hkv, D)
+        v = qkv[:, (Hq + Hkv) * D:].view(T, Hkv, D)
+        q = r(rope(q, pos, cfg.rope_theta))
+        k = r(rope(k, pos, cfg.rope_theta))
+        s = torch.einsum("qhd,khd->hqk", q, k.repeat_interleave(G, dim=1)) / (D ** 0.5)
+        s = s.masked_fill(mask.unsqueeze(0), float("-inf"))
+        a = r(torch.einsum("hqk,khd->qhd", torch.softmax(s, -1), v.repeat_interleave(G, dim=1)).reshape(T, Hq * D))
+        part = r(a @ lw["wo"].float().T + (x if rank == 0 else 0.0))
+        all_reduce(part)
+        x = r(part)
+        h = rmsnorm(x, lw["mlp_norm"].float(), cfg.eps)
+        gu = r(h @ lw["wgu"].float().T)
+        f = gu.shape[1] // 2
+        m = r(r(torch.nn.functional.silu(gu[:, :f])) * gu[:, f:])
+        part = r(m @ lw["wdown"].float().T + (x if rank == 0 else 0.0))
+        all_reduce(part)
+        x = r(part)
+    h = rmsnorm(x, w["final_norm"].float(), cfg.eps)
+    local = (h @ w["lm_head"].float().T).contiguous()
+    parts = [torch.empty_like(local) for _ in range(world)]
+    all_gather(parts, local)
+    return torch.cat(parts, dim=1)

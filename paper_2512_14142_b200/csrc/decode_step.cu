@@ -873,6 +873,7 @@ extern "C" int astraea_step_program_build(int32_t M, int32_t nph, const astraea_
       e.kind = g.epi.kind;
       if (e.kind < EPI_NONE || e.kind > EPI_ARGMAX) return ASTRAEA_EINVAL;
       e.amax = g.epi.argmax_keys_dev;
+      e.amax_off = g.epi.argmax_col_offset;
       e.residual = (const bf16*)g.epi.residual_dev;
       e.ssq_out = g.epi.ssq_out_dev;
       e.ssq_in = g.epi.ssq_in_dev;

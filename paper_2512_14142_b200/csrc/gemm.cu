@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (n0 + k < args.N) {
               const float o = v[k] * rs;
               if (args.C) crow[n0 + k] = f2bf(o);
-              best = umax64(best, argmax_key(o, n0 + k));
+              best = umax64(best, argmax_key(o, n0 + k + e.amax_off));
             }
           }
         }
@@ -692,6 +692,7 @@ int to_epi(const astraea_epilogue* in, int N, Epi* e) {
   e->kind = in->kind;
   if (in->kind < EPI_NONE || in->kind > EPI_ARGMAX) return ASTRAEA_EINVAL;
   e->amax = in->argmax_keys_dev;
+  e->amax_off = in->argmax_col_offset;
   if (e->kind == EPI_ARGMAX && !e->amax) return ASTRAEA_EINVAL;
   e->residual = (const bf16*)in->residual_dev;
   e->ssq_out = in->ssq_out_dev;

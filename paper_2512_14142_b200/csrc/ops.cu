@@ -165,6 +165,27 @@ __global__ void __launch_bounds__(1024) argmax_kernel(const bf16* __restrict__ l
   }
 }
 
+// One warp per (row, 128-column group): lane holds 4 columns.
+__global__ void row_ssq_kernel(const bf16* __restrict__ x, int rows, int dim, float* __restrict__ out) {
+  pdl_wait();
+  pdl_launch();
+  const int groups = (dim + 127) / 128;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (gw >= rows * groups) return;
+  const int row = gw / groups, g = gw % groups;
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int c = g * 128 + lane * 4 + k;
+    if (c < dim) {
+      const float v = bf2f(x[(long long)row * dim + c]);
+      s += v * v;
+    }
+  }
+  s = warp_sum(s);
+  if (lane == 0) out[(long long)g * rows + row] = s;
+}
+
 }  // namespace
 
 extern "C" int astraea_rmsnorm(const void* x, const void* r, const void* w, void* y, void* resid_out,
@@ -216,5 +237,14 @@ extern "C" int astraea_argmax(const void* logits, int32_t rows, int32_t vocab, i
   ASTRAEA_TRY(launch_k(argmax_kernel, dim3(rows), dim3(1024), 0, (cudaStream_t)stream, (const bf16*)logits,
                        (int)vocab, ids_out));
   ASTRAEA_CHECK_LAUNCH();
+  return ASTRAEA_OK;
+}
+
+extern "C" int astraea_row_ssq(const void* x, int32_t rows, int32_t dim, float* out, void* stream) {
+  if (!x || !out || rows < 0 || dim <= 0) return ASTRAEA_EINVAL;
+  if (rows == 0) return ASTRAEA_OK;
+  const long long warps = (long long)rows * ((dim + 127) / 128);
+  ASTRAEA_TRY(launch_k(row_ssq_kernel, dim3((unsigned)((warps * 32 + 255) / 256)), dim3(256), 0, (cudaStream_t)stream,
+                       (const bf16*)x, (int)rows, (int)dim, out));
   return ASTRAEA_OK;
 }

@@ -106,6 +106,7 @@ struct Epi {
   float theta;
   const float2* cs;        // optional [M][D/2] (cos, sin) table
   unsigned long long* amax;  // ARGMAX: [M] packed (value, index) keys
+  int amax_off;              // ARGMAX: column offset of this shard
 };
 
 // Greedy-sampling key: order-preserving float bits in the high word, the
@@ -214,7 +215,7 @@ __device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* 
     for (int t = 0; t < BN; ++t) {
       if (t >= M) break;
       if (a.C && fok) a.C[(long long)t * a.ldc + f] = f2bf(v[t]);
-      const unsigned long long k = warp_max64(fok ? argmax_key(v[t], f) : 0ull);
+      const unsigned long long k = warp_max64(fok ? argmax_key(v[t], f + e.amax_off) : 0ull);
       if ((row & 31) == 0) atomicMax(e.amax + t, k);
     }
     return;

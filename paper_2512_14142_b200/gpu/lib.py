@@ -53,6 +53,7 @@ class Epilogue(ctypes.Structure):
         ("rope_theta", ctypes.c_float),
         ("rope_table_dev", ctypes.c_void_p),
         ("argmax_keys_dev", ctypes.c_void_p),
+        ("argmax_col_offset", ctypes.c_int32),
     ]
 
 
@@ -145,6 +146,7 @@ SIGNATURES = {
     "astraea_debug_step_trace": (ctypes.c_int, [_vp]),
     "astraea_decode_advance": (
         ctypes.c_int, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp]),
+    "astraea_row_ssq": (ctypes.c_int, [_vp, _i32, _i32, _vp, _vp]),
     "astraea_rmsnorm": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _f32, _vp]),
     "astraea_silu_mul": (ctypes.c_int, [_vp, _vp, _i32, _i32, _vp]),
     "astraea_embedding": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i32, _vp, _vp]),

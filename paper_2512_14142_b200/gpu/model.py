@@ -96,7 +96,10 @@ class LlamaWeights:
     returns the logical (textbook) weights for the oracle.
     """
 
-    def __init__(self, cfg: LlamaConfig, device="cuda", seed: int = 0, std: float = 0.02):
+    def __init__(self, cfg: LlamaConfig, device="cuda", seed: int = 0, std: float = 0.02, embed_vocab: int = 0):
+        """``embed_vocab``: embedding rows when it differs from cfg.vocab (a
+        tensor-parallel rank keeps the whole embedding but a vocab slice of
+        the lm_head)."""
         self.cfg = cfg
         g = torch.Generator(device=device)
         g.manual_seed(seed)
@@ -111,7 +114,7 @@ class LlamaWeights:
 
         d = cfg.hidden
         ones = torch.ones(d, dtype=torch.bfloat16, device=device)
-        self.embed = w(cfg.vocab, d)
+        self.embed = w(embed_vocab or cfg.vocab, d)
         self.layers = []
         for _ in range(cfg.num_layers):
             attn_norm, mlp_norm = ones.clone(), ones.clone()
@@ -129,6 +132,33 @@ class LlamaWeights:
             })
         self.final_norm = ones.clone()
         self.lm_head = w(cfg.vocab, d)
+
+    @classmethod
+    def from_logical(cls, cfg: LlamaConfig, wd: dict, device="cuda") -> "LlamaWeights":
+        """Device weights from logical ones (the to_cpu_dict format): norms
+        folded into the following projection, gate/up interleaved."""
+        self = cls.__new__(cls)
+        self.cfg = cfg
+
+        def dv(t):
+            return t.to(device=device, dtype=torch.bfloat16).contiguous()
+
+        def fold(weight, norm):
+            return (weight.float() * norm.float()[None, :]).to(torch.bfloat16)
+
+        self.embed = dv(wd["embed"])
+        self.layers = []
+        for lw in wd["layers"]:
+            self.layers.append({
+                "attn_norm": dv(lw["attn_norm"]), "mlp_norm": dv(lw["mlp_norm"]),
+                "wqkv": dv(fold(lw["wqkv"], lw["attn_norm"])),
+                "wo": dv(lw["wo"]),
+                "wgu": dv(interleave_gate_up(fold(lw["wgu"], lw["mlp_norm"]), cfg.ffn)),
+                "wdown": dv(lw["wdown"]),
+            })
+        self.final_norm = dv(wd["final_norm"])
+        self.lm_head = dv(fold(wd["lm_head"], wd["final_norm"]))
+        return self
 
     def to_cpu_dict(self) -> dict:
         """Logical weights: un-interleaved gate/up, norms separate (the

@@ -57,8 +57,9 @@ def gemm(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None,
 
 def _epilogue(kind=L.EPI_NONE, residual=None, ssq_out=None, ssq_in=None, rms_dim=0, rms_eps=1e-5, pool=None,
               geo=None, layer=0, num_q_heads=0, positions=None, slots=None, rope_theta=0.0, rope_table=None,
-              argmax_keys=None):
+              argmax_keys=None, argmax_col_offset=0):
     e = L.Epilogue()
+    e.argmax_col_offset = argmax_col_offset
     e.kind = kind
     e.residual_dev = L.ptr(residual)
     e.ssq_out_dev = L.ptr(ssq_out)
@@ -67,6 +68,7 @@ def _epilogue(kind=L.EPI_NONE, residual=None, ssq_out=None, ssq_in=None, rms_dim
     e.rms_dim = rms_dim
     e.rms_eps = rms_eps
     e.argmax_keys_dev = L.ptr(argmax_keys)
+    e.argmax_col_offset = argmax_col_offset
     if kind == L.EPI_QKV_ROPE:
         e.pool_dev = L.ptr(pool)
         e.geo = geo
@@ -181,7 +183,7 @@ class StepWorkspace:
 
 def gemm_ex(a, w, out, kind=L.EPI_NONE, residual=None, ssq_out=None, ssq_in=None, rms_dim=0, rms_eps=1e-5,
             pool=None, geo=None, layer=0, num_q_heads=0, positions=None, slots=None, rope_theta=0.0,
-            rope_table=None, argmax_keys=None, workspace=None, stream=None):
+            rope_table=None, argmax_keys=None, workspace=None, stream=None, argmax_col_offset=0):
     """GEMM with a fused epilogue program (astraea_gemm_bf16_ex)."""
     lib = L.require_cuda()
     M, K = a.shape
@@ -212,6 +214,17 @@ def gemm_ex(a, w, out, kind=L.EPI_NONE, residual=None, ssq_out=None, ssq_in=None
         ctypes.byref(e),
         L.ptr(workspace), 0 if workspace is None else workspace.numel() * workspace.element_size(),
         _s(stream)), "gemm_bf16_ex")
+    _count()
+    return out
+
+
+def row_ssq(x, out=None, stream=None):
+    """RMSNorm statistics of x [rows][dim]: [ceil(dim/128)][rows] fp32 (astraea_row_ssq)."""
+    lib = L.require_cuda()
+    rows, dim = x.shape
+    if out is None:
+        out = torch.empty(-(-dim // 128), rows, dtype=torch.float32, device=x.device)
+    L.check(lib.astraea_row_ssq(L.ptr(x), rows, dim, L.ptr(out), _s(stream)), "row_ssq")
     _count()
     return out
 
