@@ -54,6 +54,9 @@ def parse():
                     help="KV capacity (tokens) per GPU; 3000 puts the 12-request shard under memory pressure "
                          "(preserve, swap and forced discard all occur)")
     ap.add_argument("--swap-mode", choices=("kernel", "dma"), default="kernel")
+    ap.add_argument("--cost-tables", choices=("calibrated", "b200-like"), default="calibrated",
+                    help="scheduler cost tables: measured on the B200 by tools/calibrate.py "
+                         "(profiles/r1_b200_cost_tables.json), or the survey's B200-like guess")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     return ap.parse_args()
@@ -80,14 +83,19 @@ def build_workload(args, rank, world):
     full = full[:need]
     full.sort(key=lambda r: (r.arrival_time, r.id))
     shard = full[rank::world]
-    pred = scenarios.b200_like_predictor(host)
+    if getattr(args, "cost_tables", "calibrated") == "calibrated":
+        pred, cal = scenarios.calibrated_predictor(host)
+        args.swap_tokens_per_s = float(cal["swap_bandwidth_tokens_per_s"])
+    else:
+        pred = scenarios.b200_like_predictor(host)
+        args.swap_tokens_per_s = 380_000.0
     return shard, pred
 
 
 def make_run(host, shard, pred, args, bytes_per_token):
     policy = host.make_policy("stateful-mlfq", pred, host.MlfqConfig())
     memory = host.MemoryModel(capacity_tokens=args.capacity, bytes_per_token=float(bytes_per_token),
-                              swap_bandwidth_tokens_per_s=380_000.0)
+                              swap_bandwidth_tokens_per_s=getattr(args, "swap_tokens_per_s", 380_000.0))
     config = host.SimConfig(cost_model="parallel-max", cache_mode="adaptive")
     return policy, memory, config
 
@@ -317,7 +325,7 @@ def main():
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, generated trace)",
         "config": {"workload": f"C2 {args.model} random-init, trace seed 0, {len(shard)} req/rank @ qps "
                                f"{args.qps}/rank, stateful-mlfq + adaptive KV, capacity {args.capacity} "
-                               f"tok/GPU, parallel-max, model clock",
+                               f"tok/GPU, parallel-max, model clock, {args.cost_tables} cost tables",
                    "global_requests": len(shard) * world, "parallelism": f"replicas x{world}",
                    "l2": "weights (15 GB) stream every decode step: inputs >> L2",
                    "decode_steps_per_step": work["decode_steps"], "prefill_tokens_per_step": work["prefill_tokens"],

@@ -21,11 +21,18 @@ Scenario families:
 * ``decomp/...``               -- criterion-4 grid (test_acceptance.py:239-263).
 * ``aging/<tau>``              -- aging scenario (test_acceptance.py:125-159).
 * ``noise``                    -- predictor noise sigma 0.3.
+* ``c1cal/<cap>``              -- C1 with the cost tables *measured* on the B200
+                                 (profiles/r1_b200_cost_tables.json, written by
+                                 tools/calibrate.py).
 """
 
 from __future__ import annotations
 
+import json
 import random
+from pathlib import Path
+
+CALIBRATION = Path(__file__).resolve().parent.parent / "profiles" / "r1_b200_cost_tables.json"
 
 POLICY_NAMES = ("stateful-mlfq", "fcfs", "sjf-segment", "sjf-request", "las")
 
@@ -92,6 +99,13 @@ def b200_like_predictor(ns):
                                    decode=ns.DecodeModel(0.006))
 
 
+def calibrated_predictor(ns):
+    cal = json.loads(CALIBRATION.read_text())
+    cfg = dict(cal["predictor"])
+    cfg["api_latency_means"] = ns.ServiceTimePredictor().to_config()["api_latency_means"]
+    return ns.ServiceTimePredictor.from_config(cfg), cal
+
+
 def scenario_names():
     names = [f"fig2/{p}" for p in POLICY_NAMES]
     for p in POLICY_NAMES:
@@ -99,6 +113,7 @@ def scenario_names():
             for mode in ("adaptive", "preserve"):
                 names.append(f"c1/{p}/{cap}/{mode}")
     names += [f"c1b200/{cap}" for cap in (12_000, 6_000, 3_600)]
+    names += [f"c1cal/{cap}" for cap in (12_000, 6_000, 3_600)]
     names += [f"c2/{cap}" for cap in (40_000, 12_000)]
     for seed in (0, 1):
         for p in ("stateful-mlfq", "fcfs", "sjf-segment"):
@@ -130,6 +145,12 @@ def build(ns, name):
         return (c1_trace(ns), ns.make_policy("stateful-mlfq", pred, ns.MlfqConfig()), pred,
                 ns.MemoryModel(capacity_tokens=int(parts[1]), bytes_per_token=131072.0,
                                swap_bandwidth_tokens_per_s=380_000.0),
+                ns.SimConfig(cost_model="parallel-max", cache_mode="adaptive"))
+    if fam == "c1cal":
+        pred, cal = calibrated_predictor(ns)
+        return (c1_trace(ns), ns.make_policy("stateful-mlfq", pred, ns.MlfqConfig()), pred,
+                ns.MemoryModel(capacity_tokens=int(parts[1]), bytes_per_token=float(cal["bytes_per_token"]),
+                               swap_bandwidth_tokens_per_s=float(cal["swap_bandwidth_tokens_per_s"])),
                 ns.SimConfig(cost_model="parallel-max", cache_mode="adaptive"))
     if fam == "c2":
         pred = ns.ServiceTimePredictor()

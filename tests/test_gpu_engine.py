@@ -17,7 +17,7 @@ from paper_2512_14142_b200 import host  # noqa: E402
 from paper_2512_14142_b200.gpu.engine import GpuEngine  # noqa: E402
 
 SCENARIOS = ["fig2/fcfs", "c1/stateful-mlfq/12000/adaptive", "c1b200/6000", "hetero/0/stateful-mlfq",
-             "c1/fcfs/3600/adaptive", "aging/5.0"]
+             "c1/fcfs/3600/adaptive", "aging/5.0", "c1cal/6000"]
 
 
 @pytest.mark.parametrize("name", SCENARIOS)
