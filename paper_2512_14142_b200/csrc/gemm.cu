@@ -342,6 +342,7 @@ struct ChainArgs {
   int* counters;               // [tiles] arrival counters, zero between uses
   int* phase_ctr;              // [kMaxPhases + 1] phase / kernel arrival counters, zero between launches
   int M, grid, nph;
+  int l2_pre;                  // weight tiles per CTA prefetched into L2 before griddepcontrol.wait
   SkPhase ph[kMaxPhases];
 };
 
@@ -420,6 +421,26 @@ __global__ void __launch_bounds__(kThreads, MINB)
           tma_load_2d(sa + s * A_BYTES, &maps.w[p], &full[s], (int)(u % KB) * kBK, (int)(u / KB) * kBM);
         }
         if (p == 0) {
+          // While the previous kernel (the layer's attention) finishes, keep
+          // HBM busy: prefetch the next l2_pre weight tiles of this CTA's
+          // stream (beyond the smem ring) into L2.
+          if (args.l2_pre > 0) {
+            int q = p;
+            long long uu = u0 + pre, qu1 = u1;
+            for (int k = 0; k < args.l2_pre; ++k, ++uu) {
+              while (uu >= qu1 && ++q < args.nph) {
+                long long a0, a1;
+                sk_range(args.ph[q], cta, a0, a1);
+                uu = a0;
+                qu1 = a1;
+              }
+              if (q >= args.nph) break;
+              const int qkb = args.ph[q].kbs;
+              asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(&maps.w[q]),
+                           "r"((int)(uu % qkb) * kBK), "r"((int)(uu / qkb) * kBM)
+                           : "memory");
+            }
+          }
           pdl_wait();
         } else {
           wait_phase(args.phase_ctr + p - 1, G);
@@ -849,6 +870,11 @@ static int run_chain(int M, int nph, const astraea_gemm_phase* ph, void* ws, siz
   a.M = M;
   a.grid = num_sms();
   a.nph = nph;
+  static const int l2_pre = [] {
+    const char* e = getenv("ASTRAEA_CHAIN_L2PRE");
+    return e ? atoi(e) : 0;
+  }();
+  a.l2_pre = deep ? l2_pre : 0;
   const int bn = M <= 16 ? 16 : (M <= 32 ? 32 : 64);
   for (int p = 0; p < nph; ++p) {
     const astraea_gemm_phase& q = ph[p];
