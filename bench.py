@@ -163,10 +163,15 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: run every rank on one device over gloo (NCCL needs one GPU per rank)
+    if os.environ.get("ASTRAEA_BENCH_SHARE_GPU") == "1":
+        local = 0
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local) if torch.cuda.is_available() else None
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        backend = "gloo" if (os.environ.get("ASTRAEA_BENCH_SHARE_GPU") == "1" or not torch.cuda.is_available()) \
+            else "nccl"
+        dist.init_process_group(backend)
     return rank, world, local
 
 
