@@ -57,6 +57,138 @@ struct GemmArgs {
   Epi epi;
 };
 
+// Epilogue of one 128-row x BN-column accumulator tile: thread = token row m
+// (mok: m < M), TMEM columns at lane_addr (this warp's 32 lanes), output
+// columns n_tile * BN ... (+BN). Shared by the one-CTA and the CTA-pair kernel.
+template <int BN>
+__device__ __forceinline__ void rows_epilogue(const GemmArgs& args, int m, bool mok, float rs, uint32_t lane_addr,
+                                              int tile_b) {
+  const Epi& e = args.epi;
+    bf16* crow = args.C + (long long)m * args.ldc;
+#pragma unroll 1
+  for (int g = 0; g < BN / 128; ++g) {
+    const int n_group = tile_b * BN + g * 128;    // first output column of the 128-group
+    if (e.kind == EPI_SILU || e.kind == EPI_QKV_ROPE) {
+      const int pair = (e.kind == EPI_SILU || e.D == 128) ? 2 : 1;   // chunk distance of a pair
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        if ((c / pair) % 2) continue;                 // c is the low half of its pair
+        float lo[32], hi[32];
+        tmem_ld32(lane_addr + g * 128 + c * 32, lo);
+        tmem_ld32(lane_addr + g * 128 + (c + pair) * 32, hi);
+        if (!mok || n_group >= args.N) continue;
+        if (e.kind == EPI_SILU) {
+          const int f0 = (n_group / 128) * 64 + c * 32;   // output feature of lo[0]
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            float o[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              o[q] = silu_rounded(round_bf(lo[j + q] * rs)) * round_bf(hi[j + q] * rs);
+            *reinterpret_cast<uint4*>(crow + f0 + j) = pack8(o);
+          }
+        } else {
+          // 32 consecutive columns of one head: low half hrow0.., high half +D/2
+          const int col0 = n_group + c * 32;
+          const int head = col0 / e.D, hrow0 = col0 % e.D;
+          const bool rot = head < e.Hq + e.Hkv;
+          float ylo[32], yhi[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float x0 = round_bf(lo[j] * rs), x1 = round_bf(hi[j] * rs);
+            if (rot) {
+              const float2 r = rope_cs(e, m, hrow0 + j);
+              ylo[j] = x0 * r.x - x1 * r.y;
+              yhi[j] = x1 * r.x + x0 * r.y;
+            } else {
+              ylo[j] = x0;
+              yhi[j] = x1;
+            }
+          }
+          bf16* dst = nullptr;
+          long long half_stride = e.D / 2;
+          if (head < e.Hq) {
+            dst = args.C + (long long)m * args.ldc + head * e.D + hrow0;
+          } else if (e.slots[m] >= 0) {
+            const int slot = e.slots[m];
+            const int kv = head < e.Hq + e.Hkv ? 0 : 1;
+            const int hk = head - e.Hq - kv * e.Hkv;
+            dst = e.pool + (long long)(slot / e.bt) * e.block_el +
+                  ((long long)(e.layer * 2 + kv) * e.Hkv + hk) * e.bt * e.D + (long long)(slot % e.bt) * e.D + hrow0;
+          }
+          if (dst) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              *reinterpret_cast<uint4*>(dst + j) = pack8(ylo + j);
+              *reinterpret_cast<uint4*>(dst + half_stride + j) = pack8(yhi + j);
+            }
+          }
+        }
+      }
+      continue;
+    }
+    if (e.kind == EPI_ARGMAX) {
+      unsigned long long best = 0ull;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        float v[32];
+        tmem_ld32(lane_addr + g * 128 + c * 32, v);
+        const int n0 = n_group + c * 32;
+        if (!mok) continue;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          if (n0 + k < args.N) {
+            const float o = v[k] * rs;
+            if (args.C) crow[n0 + k] = f2bf(o);
+            best = umax64(best, argmax_key(o, n0 + k + e.amax_off));
+          }
+        }
+      }
+      if (mok) atomicMax(e.amax + m, best);
+      continue;
+    }
+    float ssq = 0.f;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      float v[32];
+      tmem_ld32(lane_addr + g * 128 + c * 32, v);
+      const int n0 = n_group + c * 32;
+      if (!mok || n0 >= args.N) continue;
+      bf16* dst = crow + n0;
+      const bf16* res = e.kind == EPI_RESIDUAL ? e.residual + (long long)m * args.ldc + n0 : nullptr;
+      if (n0 + 32 <= args.N) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float o[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) o[k] = v[q * 8 + k] * rs;
+          if (res) {
+            float r[8];
+            unpack8(*reinterpret_cast<const uint4*>(res + q * 8), r);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) o[k] += r[k];
+          }
+          const uint4 packed = pack8(o);
+          *reinterpret_cast<uint4*>(dst + q * 8) = packed;
+          float ob[8];
+          unpack8(packed, ob);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) ssq += ob[k] * ob[k];
+        }
+      } else {
+        for (int k = 0; k < 32 && n0 + k < args.N; ++k) {
+          float o = v[k] * rs;
+          if (res) o += bf2f(res[k]);
+          const bf16 ob = f2bf(o);
+          dst[k] = ob;
+          ssq += bf2f(ob) * bf2f(ob);
+        }
+      }
+    }
+    if (e.ssq_out && mok && n_group < args.N) e.ssq_out[(long long)(n_group / 128) * args.M + m] = ssq;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // kRows (prefill): one 128 x BN output tile per CTA. Epilogue thread = one
 // token row; columns are processed in 128-column groups (4 TMEM chunks of
@@ -145,133 +277,184 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_wait(done, 0);
     tc_fence_after();
     const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
-    bf16* crow = args.C + (long long)m * args.ldc;
-#pragma unroll 1
-    for (int g = 0; g < BN / 128; ++g) {
-      const int n_group = tile_b * BN + g * 128;    // first output column of the 128-group
-      if (e.kind == EPI_SILU || e.kind == EPI_QKV_ROPE) {
-        const int pair = (e.kind == EPI_SILU || e.D == 128) ? 2 : 1;   // chunk distance of a pair
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          if ((c / pair) % 2) continue;                 // c is the low half of its pair
-          float lo[32], hi[32];
-          tmem_ld32(lane_addr + g * 128 + c * 32, lo);
-          tmem_ld32(lane_addr + g * 128 + (c + pair) * 32, hi);
-          if (!mok || n_group >= args.N) continue;
-          if (e.kind == EPI_SILU) {
-            const int f0 = (n_group / 128) * 64 + c * 32;   // output feature of lo[0]
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              float o[8];
-#pragma unroll
-              for (int q = 0; q < 8; ++q)
-                o[q] = silu_rounded(round_bf(lo[j + q] * rs)) * round_bf(hi[j + q] * rs);
-              *reinterpret_cast<uint4*>(crow + f0 + j) = pack8(o);
-            }
-          } else {
-            // 32 consecutive columns of one head: low half hrow0.., high half +D/2
-            const int col0 = n_group + c * 32;
-            const int head = col0 / e.D, hrow0 = col0 % e.D;
-            const bool rot = head < e.Hq + e.Hkv;
-            float ylo[32], yhi[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float x0 = round_bf(lo[j] * rs), x1 = round_bf(hi[j] * rs);
-              if (rot) {
-                const float2 r = rope_cs(e, m, hrow0 + j);
-                ylo[j] = x0 * r.x - x1 * r.y;
-                yhi[j] = x1 * r.x + x0 * r.y;
-              } else {
-                ylo[j] = x0;
-                yhi[j] = x1;
-              }
-            }
-            bf16* dst = nullptr;
-            long long half_stride = e.D / 2;
-            if (head < e.Hq) {
-              dst = args.C + (long long)m * args.ldc + head * e.D + hrow0;
-            } else if (e.slots[m] >= 0) {
-              const int slot = e.slots[m];
-              const int kv = head < e.Hq + e.Hkv ? 0 : 1;
-              const int hk = head - e.Hq - kv * e.Hkv;
-              dst = e.pool + (long long)(slot / e.bt) * e.block_el +
-                    ((long long)(e.layer * 2 + kv) * e.Hkv + hk) * e.bt * e.D + (long long)(slot % e.bt) * e.D + hrow0;
-            }
-            if (dst) {
-#pragma unroll
-              for (int j = 0; j < 32; j += 8) {
-                *reinterpret_cast<uint4*>(dst + j) = pack8(ylo + j);
-                *reinterpret_cast<uint4*>(dst + half_stride + j) = pack8(yhi + j);
-              }
-            }
-          }
-        }
-        continue;
-      }
-      if (e.kind == EPI_ARGMAX) {
-        unsigned long long best = 0ull;
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          float v[32];
-          tmem_ld32(lane_addr + g * 128 + c * 32, v);
-          const int n0 = n_group + c * 32;
-          if (!mok) continue;
-#pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            if (n0 + k < args.N) {
-              const float o = v[k] * rs;
-              if (args.C) crow[n0 + k] = f2bf(o);
-              best = umax64(best, argmax_key(o, n0 + k + e.amax_off));
-            }
-          }
-        }
-        if (mok) atomicMax(e.amax + m, best);
-        continue;
-      }
-      float ssq = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        float v[32];
-        tmem_ld32(lane_addr + g * 128 + c * 32, v);
-        const int n0 = n_group + c * 32;
-        if (!mok || n0 >= args.N) continue;
-        bf16* dst = crow + n0;
-        const bf16* res = e.kind == EPI_RESIDUAL ? e.residual + (long long)m * args.ldc + n0 : nullptr;
-        if (n0 + 32 <= args.N) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float o[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) o[k] = v[q * 8 + k] * rs;
-            if (res) {
-              float r[8];
-              unpack8(*reinterpret_cast<const uint4*>(res + q * 8), r);
-#pragma unroll
-              for (int k = 0; k < 8; ++k) o[k] += r[k];
-            }
-            const uint4 packed = pack8(o);
-            *reinterpret_cast<uint4*>(dst + q * 8) = packed;
-            float ob[8];
-            unpack8(packed, ob);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) ssq += ob[k] * ob[k];
-          }
-        } else {
-          for (int k = 0; k < 32 && n0 + k < args.N; ++k) {
-            float o = v[k] * rs;
-            if (res) o += bf2f(res[k]);
-            const bf16 ob = f2bf(o);
-            dst[k] = ob;
-            ssq += bf2f(ob) * bf2f(ob);
-          }
-        }
-      }
-      if (e.ssq_out && mok && n_group < args.N) e.ssq_out[(long long)(n_group / 128) * args.M + m] = ssq;
-    }
+    rows_epilogue<BN>(args, m, mok, rs, lane_addr, tile_b);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
+}
+
+// ---------------------------------------------------------------------------
+// Prefill GEMM on a CTA pair (tcgen05 cta_group::2), persistent.
+//
+// A cluster of two CTAs on one TPC computes 256 x 256 output tiles: CTA r
+// stages rows [128 r, 128 r + 128) of the A tile and of the W tile, the
+// leader issues tcgen05.mma.cta_group::2 (M = 256, N = 256) reading both
+// CTAs' shared memory, and each CTA's TMEM receives its 128 rows. Per CTA a
+// stage is 32 KB (instead of 48 KB for a one-CTA 128 x 256 tile), so six
+// stages fit and cover the TMA latency at tensor-core rate; the two 256-column
+// accumulators (all 512 TMEM columns) let the epilogue of one tile overlap
+// the main loop of the next. Tiles are walked M-fastest so consecutive tiles
+// of a pair reuse the same weight columns from L2.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* smem, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                 int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(smem_u32(smem)),
+      "l"(map), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {   // to the same barrier in both CTAs
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
+template <int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                     const __grid_constant__ GemmArgs args) {
+  constexpr int HALF = 128;                    // rows of A and of W staged per CTA
+  constexpr int A_BYTES = HALF * kBK * 2;
+  constexpr int B_BYTES = HALF * kBK * 2;
+  constexpr uint32_t TMEM_COLS = 512;          // two 256-column accumulators
+  constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
+                             ((uint32_t)(256 >> 4) << 24);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int TM = (args.M + 255) / 256, TN = (args.N + 255) / 256, tiles = TM * TN;
+  const int KB = (args.K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);   // 4 epilogue warps x 2 CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_launch();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      pdl_wait();
+      int idx = 0;
+      for (int t = pair; t < tiles; t += npairs) {
+        const int tm = t % TM, tn = t / TM;
+        for (int kb = 0; kb < KB; ++kb, ++idx) {
+          const int s = idx % STAGES;
+          if (idx >= STAGES) mbar_wait(&empty[s], ((idx / STAGES) - 1) & 1);
+          if (leader) mbar_arrive_expect_tx(&full[s], 2 * (A_BYTES + B_BYTES));
+          const uint32_t bar = mapa_shared(smem_u32(&full[s]), 0);   // the leader's barrier counts both CTAs
+          tma_load_2d_pair(sa + s * A_BYTES, &map_a, bar, kb * kBK, tm * 256 + (int)rank * HALF);
+          tma_load_2d_pair(sb + s * B_BYTES, &map_b, bar, kb * kBK, tn * 256 + (int)rank * HALF);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      int i = 0, lt = 0;
+      for (int t = pair; t < tiles; t += npairs, ++lt) {
+        const int buf = lt & 1;
+        if (lt >= 2) mbar_wait(&tempty[buf], ((lt >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t acc = tmem + buf * 256;
+        for (int kb = 0; kb < KB; ++kb, ++i) {
+          const int s = i % STAGES;
+          mbar_wait(&full[s], (i / STAGES) & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint64_t da = smem_desc_sw128(sa + s * A_BYTES);
+            const uint64_t db = smem_desc_sw128(sb + s * B_BYTES);
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k) mma_bf16_pair(acc, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            mma_commit_pair(&empty[s]);
+          }
+          __syncwarp();
+        }
+        if (lane == 0) mma_commit_pair(&tfull[buf]);
+        __syncwarp();
+      }
+    }
+  } else {
+    pdl_wait();
+    const Epi& e = args.epi;
+    const int quarter = warp & 3;
+    const uint32_t tempty_leader[2] = {mapa_shared(smem_u32(&tempty[0]), 0), mapa_shared(smem_u32(&tempty[1]), 0)};
+    int lt = 0;
+    for (int t = pair; t < tiles; t += npairs, ++lt) {
+      const int tm = t % TM, tn = t / TM;
+      const int buf = lt & 1;
+      const int m = tm * 256 + (int)rank * HALF + quarter * 32 + lane;
+      const bool mok = m < args.M;
+      const float rs = (e.ssq_in && mok) ? rms_scale(e, args.M, m) : 1.f;
+      mbar_wait(&tfull[buf], (lt >> 1) & 1);
+      tc_fence_after();
+      rows_epilogue<256>(args, m, mok, rs, tmem + ((uint32_t)(quarter * 32) << 16) + buf * 256, tn);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(tempty_leader[buf]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
 // ---------------------------------------------------------------------------
@@ -653,6 +836,44 @@ int launch_rows(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a,
   return 0;
 }
 
+template <int STAGES>
+int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, cudaStream_t st) {
+  auto kern = gemm_pair_kernel<STAGES>;
+  constexpr size_t smem = 1024 + (size_t)STAGES * (2 * 128 * kBK * 2) + (2 * STAGES + 4) * 8 + 16;
+  static bool attr = false;
+  if (!attr) {
+    ASTRAEA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const int tiles = ((a.M + 255) / 256) * ((a.N + 255) / 256);
+  const int pairs = std::max(1, std::min(tiles, num_sms() / 2));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  ASTRAEA_TRY(cudaLaunchKernelEx(&cfg, kern, ma, mb, a));
+  return 0;
+}
+
+bool pair_gemm_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ASTRAEA_GEMM_PAIR");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 constexpr int kColsMaxM = 64;
 
 struct SkPlan {
@@ -952,6 +1173,11 @@ extern "C" int astraea_gemm_bf16_ex(const void* A, int32_t lda, const void* W, i
   a.K = K;
   a.ldc = ldc;
   a.epi = e;
+  if (pair_gemm_enabled()) {
+    if ((rc = make_map(&ma, A, M, K, lda, 128))) return rc;
+    if ((rc = make_map(&mb, W, N, K, ldw, 128))) return rc;
+    return launch_pair<6>(ma, mb, a, st);
+  }
   const int bn = (N % 256 == 0 && (long long)((M + kBM - 1) / kBM) * (N / 256) >= num_sms()) ? 256 : 128;
   if ((rc = make_map(&ma, A, M, K, lda, kBM))) return rc;
   if ((rc = make_map(&mb, W, N, K, ldw, bn))) return rc;
