@@ -449,3 +449,27 @@ def test_gemm_chain_equals_separate_gemms(M):
     assert torch.equal(outs[True][0], outs[False][0])
     assert torch.equal(outs[True][1], outs[False][1])
     assert torch.equal(outs[True][2], outs[False][2])
+
+
+@pytest.mark.parametrize("M,N,K", [(600, 640, 320), (4096, 2048, 512), (129, 1024, 200), (257, 6144, 4096)])
+def test_pair_gemm_shapes_match_fp32(M, N, K):
+    """The CTA-pair prefill GEMM (cta_group::2): partial 256-row / 256-column
+    tiles, K tails (TMA zero fill), more tiles than pairs (persistent,
+    double-buffered TMEM)."""
+    g = torch.Generator(device=DEV).manual_seed(M + N + K)
+    a = torch.randn(M, K, generator=g, device=DEV).bfloat16()
+    w = (torch.randn(N, K, generator=g, device=DEV) * 0.05).bfloat16()
+    res = torch.randn(M, N, generator=g, device=DEV).bfloat16()
+    out = res.clone()
+    ops.gemm(a, w, out, residual=out)
+    torch.cuda.synchronize()
+    ref = a.float() @ w.float().T + res.float()
+    assert rel_err(out, ref) < 1e-2
+
+
+def test_row_ssq_matches_torch():
+    x = torch.randn(37, 4096, device=DEV).bfloat16()
+    s = ops.row_ssq(x)
+    torch.cuda.synchronize()
+    ref = x.float().view(37, 32, 128).pow(2).sum(-1).T
+    assert s.shape == (32, 37) and torch.allclose(s, ref, rtol=1e-4, atol=1e-3)
