@@ -50,19 +50,28 @@ using namespace astraea::tc;
 namespace {
 
 constexpr int kThreads = 192;
+constexpr int kMaxPhases = 4;   // GEMMs per chain launch
 
 struct GemmArgs {
   bf16* C;
   int M, N, K, ldc;
   Epi epi;
+  // CTA-pair kernel split-K (splits > 1 only when tiles * splits <= pairs):
+  int splits;
+  unsigned long long* part;    // [tiles][splits - 1][2 CTAs][128][256] tagged fp32 partials
+  int* ctr;                    // workspace counters: [kMaxPhases] exit, [kMaxPhases + 1] launch epoch
 };
 
 // Epilogue of one 128-row x BN-column accumulator tile: thread = token row m
 // (mok: m < M), TMEM columns at lane_addr (this warp's 32 lanes), output
 // columns n_tile * BN ... (+BN). Shared by the one-CTA and the CTA-pair kernel.
-template <int BN>
+struct NoFix {
+  __device__ __forceinline__ void operator()(float*, int) const {}
+};
+
+template <int BN, class Fix = NoFix>
 __device__ __forceinline__ void rows_epilogue(const GemmArgs& args, int m, bool mok, float rs, uint32_t lane_addr,
-                                              int tile_b) {
+                                              int tile_b, const Fix& fix = Fix()) {
   const Epi& e = args.epi;
     bf16* crow = args.C + (long long)m * args.ldc;
 #pragma unroll 1
@@ -76,6 +85,8 @@ __device__ __forceinline__ void rows_epilogue(const GemmArgs& args, int m, bool 
         float lo[32], hi[32];
         tmem_ld32(lane_addr + g * 128 + c * 32, lo);
         tmem_ld32(lane_addr + g * 128 + (c + pair) * 32, hi);
+        fix(lo, g * 128 + c * 32);
+        fix(hi, g * 128 + (c + pair) * 32);
         if (!mok || n_group >= args.N) continue;
         if (e.kind == EPI_SILU) {
           const int f0 = (n_group / 128) * 64 + c * 32;   // output feature of lo[0]
@@ -133,6 +144,7 @@ __device__ __forceinline__ void rows_epilogue(const GemmArgs& args, int m, bool 
       for (int c = 0; c < 4; ++c) {
         float v[32];
         tmem_ld32(lane_addr + g * 128 + c * 32, v);
+        fix(v, g * 128 + c * 32);
         const int n0 = n_group + c * 32;
         if (!mok) continue;
 #pragma unroll
@@ -152,6 +164,7 @@ __device__ __forceinline__ void rows_epilogue(const GemmArgs& args, int m, bool 
     for (int c = 0; c < 4; ++c) {
       float v[32];
       tmem_ld32(lane_addr + g * 128 + c * 32, v);
+      fix(v, g * 128 + c * 32);
       const int n0 = n_group + c * 32;
       if (!mok || n0 >= args.N) continue;
       bf16* dst = crow + n0;
@@ -337,6 +350,29 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_cluster) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
 
+// Partial sums of the other K-splits of a tile, added to each 32-column chunk
+// the finisher (split 0) loads from TMEM: self-validating 64-bit words
+// (fp32 bits | tag << 32), one spin per word.
+struct PairSplitFix {
+  const unsigned long long* base;   // (tile, split 1, this CTA) row `row`
+  long long stride;                 // between splits
+  int extra;                        // splits - 1
+  unsigned tag;
+  __device__ __forceinline__ void operator()(float* v, int col) const {
+    for (int s = 0; s < extra; ++s) {
+      const unsigned long long* p = base + s * stride + col;
+      unsigned long long w[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) w[j] = ld_relaxed_u64(p + j);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        while ((unsigned)(w[j] >> 32) != tag) w[j] = ld_relaxed_u64(p + j);
+        v[j] += __uint_as_float((unsigned)w[j]);
+      }
+    }
+  }
+};
+
 template <int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
@@ -363,6 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const int TM = (args.M + 255) / 256, TN = (args.N + 255) / 256, tiles = TM * TN;
   const int KB = (args.K + kBK - 1) / kBK;
+  const int S = args.splits, units = tiles * S;   // unit = (tile, K-split)
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
@@ -393,9 +430,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       pdl_wait();
       int idx = 0;
-      for (int t = pair; t < tiles; t += npairs) {
+      for (int u = pair; u < units; u += npairs) {
+        const int t = u / S, sp = u % S;
         const int tm = t % TM, tn = t / TM;
-        for (int kb = 0; kb < KB; ++kb, ++idx) {
+        const int k0 = sp * KB / S, k1 = (sp + 1) * KB / S;
+        for (int kb = k0; kb < k1; ++kb, ++idx) {
           const int s = idx % STAGES;
           if (idx >= STAGES) mbar_wait(&empty[s], ((idx / STAGES) - 1) & 1);
           if (leader) mbar_arrive_expect_tx(&full[s], 2 * (A_BYTES + B_BYTES));
@@ -408,12 +447,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (leader) {
       int i = 0, lt = 0;
-      for (int t = pair; t < tiles; t += npairs, ++lt) {
+      for (int u = pair; u < units; u += npairs, ++lt) {
+        const int sp = u % S;
+        const int k0 = sp * KB / S, k1 = (sp + 1) * KB / S;
         const int buf = lt & 1;
         if (lt >= 2) mbar_wait(&tempty[buf], ((lt >> 1) - 1) & 1);
         tc_fence_after();
         const uint32_t acc = tmem + buf * 256;
-        for (int kb = 0; kb < KB; ++kb, ++i) {
+        for (int kb = k0; kb < k1; ++kb, ++i) {
           const int s = i % STAGES;
           mbar_wait(&full[s], (i / STAGES) & 1);
           tc_fence_after();
@@ -421,7 +462,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t da = smem_desc_sw128(sa + s * A_BYTES);
             const uint64_t db = smem_desc_sw128(sb + s * B_BYTES);
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k) mma_bf16_pair(acc, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            for (int k = 0; k < kBK / 16; ++k)
+              mma_bf16_pair(acc, da + 2 * k, db + 2 * k, idesc, (kb != k0 || k != 0) ? 1u : 0u);
             mma_commit_pair(&empty[s]);
           }
           __syncwarp();
@@ -435,16 +477,41 @@ __global__ void __launch_bounds__(kThreads, 1)
     const Epi& e = args.epi;
     const int quarter = warp & 3;
     const uint32_t tempty_leader[2] = {mapa_shared(smem_u32(&tempty[0]), 0), mapa_shared(smem_u32(&tempty[1]), 0)};
+    const unsigned tag = S > 1 ? (((unsigned)__ldcg(args.ctr + kMaxPhases + 1) + 1u) << 3) | 7u : 0u;
+    const int row_local = quarter * 32 + lane;
+    constexpr long long kPartCta = (long long)HALF * 256;   // words per CTA partial
     int lt = 0;
-    for (int t = pair; t < tiles; t += npairs, ++lt) {
+    for (int u = pair; u < units; u += npairs, ++lt) {
+      const int t = u / S, sp = u % S;
       const int tm = t % TM, tn = t / TM;
       const int buf = lt & 1;
-      const int m = tm * 256 + (int)rank * HALF + quarter * 32 + lane;
+      const int m = tm * 256 + (int)rank * HALF + row_local;
       const bool mok = m < args.M;
-      const float rs = (e.ssq_in && mok) ? rms_scale(e, args.M, m) : 1.f;
+      const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + buf * 256;
       mbar_wait(&tfull[buf], (lt >> 1) & 1);
       tc_fence_after();
-      rows_epilogue<256>(args, m, mok, rs, tmem + ((uint32_t)(quarter * 32) << 16) + buf * 256, tn);
+      if (sp > 0) {
+        // contributor: publish this split's accumulator rows as tagged partials
+        unsigned long long* p =
+            args.part + (((long long)t * (S - 1) + (sp - 1)) * 2 + rank) * kPartCta + (long long)row_local * 256;
+        for (int c = 0; c < 8; ++c) {
+          float v[32];
+          tmem_ld32(taddr + c * 32, v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            st_relaxed_u64(p + c * 32 + j,
+                           (unsigned long long)__float_as_uint(v[j]) | ((unsigned long long)tag << 32));
+        }
+      } else {
+        const float rs = (e.ssq_in && mok) ? rms_scale(e, args.M, m) : 1.f;
+        if (S > 1) {
+          PairSplitFix fix{args.part + ((long long)t * (S - 1) * 2 + rank) * kPartCta + (long long)row_local * 256,
+                           2 * kPartCta, S - 1, tag};
+          rows_epilogue<256>(args, m, mok, rs, taddr, tn, fix);
+        } else {
+          rows_epilogue<256>(args, m, mok, rs, taddr, tn);
+        }
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(tempty_leader[buf]);
@@ -455,6 +522,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   cluster_sync_all();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  if (threadIdx.x == 0 && args.ctr) {
+    // the last CTA to leave advances the workspace's launch epoch (partial tags)
+    if (atom_add_acq_rel(args.ctr + kMaxPhases, 1) == (int)gridDim.x - 1) {
+      args.ctr[kMaxPhases] = 0;
+      args.ctr[kMaxPhases + 1] += 1;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -493,7 +567,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 // drains -- the same trick PDL plays at kernel boundaries (phase 0 waits on
 // griddepcontrol.wait instead).
 // ---------------------------------------------------------------------------
-constexpr int kMaxPhases = 4;
 
 struct SkPhase {
   bf16* C;
@@ -846,7 +919,7 @@ int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a,
     attr = true;
   }
   const int tiles = ((a.M + 255) / 256) * ((a.N + 255) / 256);
-  const int pairs = std::max(1, std::min(tiles, num_sms() / 2));
+  const int pairs = std::max(1, std::min(tiles * a.splits, num_sms() / 2));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(kThreads);
@@ -1063,8 +1136,36 @@ static size_t chain_ws_bytes(int M, int nph, const astraea_gemm_phase* ph) {
   return kCounterBytes + kPhaseBytes + part;
 }
 
+// K-splits of the CTA-pair GEMM: only when its tiles leave pairs idle (small
+// M, e.g. a short prefill), at most one unit per pair (so a split's finisher
+// never waits on work queued behind it), >= 4 k-blocks per split.
+// Experimental (ASTRAEA_PAIR_SPLITK=1): measured 2-4x *slower* at M <= 256 on
+// B200 -- the fp32 partial exchange through L2 (256 KB per CTA and split)
+// costs more than the idle pairs -- so off by default.
+static int pair_splits(int M, int N, int K) {
+  static const bool on = [] {
+    const char* e = getenv("ASTRAEA_PAIR_SPLITK");
+    return e && e[0] == '1';
+  }();
+  if (!on) return 1;
+  const int tiles = ((M + 255) / 256) * ((N + 255) / 256);
+  const int pairs = num_sms() / 2;
+  const int kb = (K + kBK - 1) / kBK;
+  if (tiles >= pairs) return 1;
+  return std::max(1, std::min(std::min(pairs / tiles, kb / 4), 8));
+}
+static size_t pair_partial_bytes(int M, int N, int K) {
+  const int S = pair_splits(M, N, K);
+  const long long tiles = (long long)((M + 255) / 256) * ((N + 255) / 256);
+  return (size_t)tiles * (S - 1) * 2 * 128 * 256 * sizeof(unsigned long long);
+}
+
 extern "C" size_t astraea_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K) {
-  if (M <= 0 || M > kColsMaxM || N <= 0 || K <= 0) return 0;
+  if (M <= 0 || N <= 0 || K <= 0) return 0;
+  if (M > kColsMaxM) {
+    const size_t p = pair_partial_bytes(M, N, K);
+    return p ? kCounterBytes + kPhaseBytes + p : 0;
+  }
   return kCounterBytes + kPhaseBytes + partial_bytes(M, sk_plan(M, N, K));
 }
 
@@ -1166,7 +1267,7 @@ extern "C" int astraea_gemm_bf16_ex(const void* A, int32_t lda, const void* W, i
     return run_chain(M, 1, &ph, ws, ws_bytes, false, st);
   }
   CUtensorMap ma, mb;
-  GemmArgs a;
+  GemmArgs a{};
   a.C = (bf16*)C;
   a.M = M;
   a.N = N;
@@ -1176,6 +1277,17 @@ extern "C" int astraea_gemm_bf16_ex(const void* A, int32_t lda, const void* W, i
   if (pair_gemm_enabled()) {
     if ((rc = make_map(&ma, A, M, K, lda, 128))) return rc;
     if ((rc = make_map(&mb, W, N, K, ldw, 128))) return rc;
+    a.splits = pair_splits(M, N, K);
+    a.part = nullptr;
+    a.ctr = nullptr;
+    if (a.splits > 1) {
+      if (ws && ws_bytes >= kCounterBytes + kPhaseBytes + pair_partial_bytes(M, N, K)) {
+        a.ctr = (int*)((char*)ws + kCounterBytes);
+        a.part = (unsigned long long*)((char*)ws + kCounterBytes + kPhaseBytes);
+      } else {
+        a.splits = 1;   // no workspace: unsplit (fewer pairs busy, same result)
+      }
+    }
     return launch_pair<6>(ma, mb, a, st);
   }
   const int bn = (N % 256 == 0 && (long long)((M + kBM - 1) / kBM) * (N / 256) >= num_sms()) ? 256 : 128;

@@ -203,7 +203,9 @@ class LlamaRunner:
         shapes = [(cfg.qkv_dim, d), (d, cfg.num_q_heads * cfg.head_dim), (2 * cfg.ffn, d), (d, cfg.ffn),
                   (cfg.vocab, d)]
         lib = L.load()
-        need = max(lib.astraea_gemm_workspace_bytes(64, n, k) for n, k in shapes)
+        # decode (M <= 64: stream-K partials) and short prefills (CTA-pair K-split partials)
+        need = max(lib.astraea_gemm_workspace_bytes(m, n, k) for n, k in shapes
+                   for m in (64, 65, 128, 192, 256, 384, 512, 768, 1024))
         # (a chain's workspace is the max over its phases: the same bound)
         # split-K workspace (partials + arrival counters): zero-filled once,
         # the kernel resets its counters.
