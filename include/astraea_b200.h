@@ -256,6 +256,29 @@ ASTRAEA_API size_t astraea_gemm_chain_workspace_bytes(int32_t M, int32_t nphases
                                           const astraea_gemm_phase* phases);
 ASTRAEA_API int astraea_gemm_chain(int32_t M, int32_t nphases, const astraea_gemm_phase* phases,
                        void* workspace_dev, size_t workspace_bytes, void* stream);
+/* A layer's decode attention followed by its chained GEMMs, in ONE launch:
+ * the epilogue warps of every CTA run the paged decode attention of `attn`
+ * (tensor cores, splits merged in CTA order) while the weight producer
+ * already streams phase 0's weights; phase 0's A must be attn->out_dev
+ * ([M][num_q_heads * head_dim]). Replaces the separate decode-attention
+ * launch of K4 (simulator.py:337); same workspace as astraea_gemm_chain.
+ * Supported: head_dim 128 with 4 q heads per kv head, head_dim 64 with 2 or 4. */
+typedef struct {
+  const void* pool_dev;
+  astraea_kv_geometry geo;
+  int32_t layer;
+  int32_t num_q_heads;
+  const void* q_dev;
+  int32_t q_row_stride;
+  const int32_t* table_dev;
+  int32_t max_blocks;
+  const int32_t* ctx_dev;
+  float scale;
+  void* out_dev;
+} astraea_attn_phase;
+ASTRAEA_API int astraea_gemm_chain_attn(int32_t M, const astraea_attn_phase* attn, int32_t nphases,
+                           const astraea_gemm_phase* phases, void* workspace_dev, size_t workspace_bytes,
+                           void* stream);
 ASTRAEA_API int astraea_gemm_bf16_ex(const void* A_dev, int32_t lda, const void* W_dev, int32_t ldw,
                          void* C_dev, int32_t ldc, int32_t M, int32_t N, int32_t K,
                          const astraea_epilogue* epilogue, void* workspace_dev,
@@ -315,7 +338,7 @@ ASTRAEA_API int astraea_step_launch(int32_t M, int32_t nphases, const void* prog
                         int32_t l2_lookahead, void* stream);
 
 /* Diagnostics: when buf != NULL, each following decode (stream-K / chain)
- * GEMM launch writes per-CTA %globaltimer stamps [grid][16] into the next of
+ * GEMM launch writes per-CTA %globaltimer stamps [grid][32] into the next of
  * `slots` slots of `slot_stride` u64 each: [0] entry, [1+p] activations of
  * phase p released, [5+p] epilogue of phase p done, [9] MMAs done, [10] exit.
  * Pass NULL to disable. */

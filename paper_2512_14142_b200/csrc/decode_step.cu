@@ -79,9 +79,8 @@ struct AttnDesc {
   bf16* out;            // [M][Hq*D]
   float scale_log2;
   const int* qkv_flags; // tile flags of the QKV phase (128 features per tile)
-  int* seq_ctr;         // [M][Hkv] split arrival counters
   int* head_ctr;        // [Hkv] finished rows per head
-  float* ws;            // [4*grid][2][G][D+2] split partials
+  unsigned long long* ws;   // [grid][G][D+2] tagged split partials
   int min_pages;
 };
 
@@ -131,9 +130,6 @@ __device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gp
 __device__ __forceinline__ bool flag_set(const int* flags, int i, int epoch) {
   return ld_relaxed(flags + i * kFlagStride) == epoch;
 }
-__device__ __forceinline__ void l2_prefetch_bulk(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ void spin_flag(const int* flags, int i, int epoch) {
   int ns = 64;
   while (!flag_set(flags, i, epoch)) {
@@ -151,11 +147,6 @@ __device__ __forceinline__ void set_flag(int* flags, int i, int epoch) {
 #else
   st_release(flags + i * kFlagStride, epoch);
 #endif
-}
-__device__ __forceinline__ int warp_max_i(int v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
 }
 
 
@@ -208,227 +199,52 @@ __device__ __forceinline__ void attn_wait_qkv(const AttnDesc& A, int h, int epoc
   __syncwarp();
 }
 
-// One layer's attention by the 4 epilogue warps of every CTA. The (row, kv
-// head) sequences' pages are split evenly over the CTAs; inside a CTA the
-// four warps take every fourth page of the CTA's piece and merge in shared
-// memory, so each sequence has at most one partial per CTA. The last CTA to
-// finish a split sequence merges the partials (CTA order: deterministic); the
-// kv head's flag is raised when all M rows of that head are written.
+// The step kernel's attention phase: attn_cta_phase (attn_mma.cuh) with the
+// QKV tile flags as the per-head dependency and the kv-head flag as output.
 template <int D, int G>
-__device__ __noinline__ void attn_phase(const MkPhase& P, int epoch, int cta, int grid, int warp, int lane, bf16* vs_all,
-                                        int* out_flags, unsigned long long* atr) {
-  // atr (diagnostics, may be null): this warp's first piece: [0] entry,
-  // [1] q/k/v flags seen, [2] q loaded, [3] pages done, [4] CTA merge +
-  // partial published, [5] split merge done, [6] output published, [7] exit
-  auto mark = [&](int k, bool first) {
-    if (atr && first && lane == 0) atr[k] = gtimer();
-  };
-  mark(0, true);
-  const AttnDesc& A = P.attn;
-  const int M = P.M, Hkv = A.Hkv;
-  const int et = warp * 32 + lane;
-  bf16* vs = vs_all + warp * (kAttnSmem / 2);
-  // pages per row (retired rows count one empty page so that every (row, head) is written)
-  int pg0 = 0, pg1 = 0;
-  if (lane < M) pg0 = max(1, (__ldg(A.ctx + lane) + kBT - 1) / kBT);
-  if (lane + 32 < M) pg1 = max(1, (__ldg(A.ctx + lane + 32) + kBT - 1) / kBT);
-  int s0 = pg0, s1 = pg1;   // inclusive scan over rows 0..63 (lane holds rows lane and lane+32)
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int a = __shfl_up_sync(0xffffffffu, s0, o), c = __shfl_up_sync(0xffffffffu, s1, o);
-    if (lane >= o) {
-      s0 += a;
-      s1 += c;
-    }
-  }
-  s1 += __shfl_sync(0xffffffffu, s0, 31);
-  const int total_pages = __shfl_sync(0xffffffffu, s1, 31);
-  const int U = Hkv * total_pages;
-  // pages per CTA: cover the SMs, >= 4 * min_pages, <= 32 parts per sequence
-  const int maxpg = warp_max_i(max(pg0, pg1));
-  const int qc = max(max(4 * A.min_pages, (U + grid - 1) / grid), (maxpg + 30) / 31);
-  const int my0 = cta * qc, my1 = min(U, my0 + qc);
-  const int ex0 = s0 - pg0, ex1 = s1 - pg1;   // exclusive prefixes of rows lane, lane+32
-  auto resolve = [&](int cur, int& b, int& h, int& seq0, int& seq1, int& pe) {
-    const unsigned b0 = __ballot_sync(0xffffffffu, lane < M && Hkv * ex0 <= cur);
-    const unsigned b1 = __ballot_sync(0xffffffffu, lane + 32 < M && Hkv * ex1 <= cur);
-    b = __popc(b0) + __popc(b1) - 1;
-    const int exb = __shfl_sync(0xffffffffu, b < 32 ? ex0 : ex1, b & 31);
-    const int pgb = __shfl_sync(0xffffffffu, b < 32 ? pg0 : pg1, b & 31);
-    const int row_start = Hkv * exb;
-    h = (cur - row_start) / pgb;
-    seq0 = row_start + h * pgb;
-    seq1 = seq0 + pgb;
-    pe = min(my1, seq1);
-  };
-  // L2 prefetch of this warp's K/V pages before waiting for the QKV flags
-  for (int cur = my0; cur < my1;) {
-    int b, h, seq0, seq1, pe;
-    resolve(cur, b, h, seq0, seq1, pe);
-    const int ctx_b = __ldg(A.ctx + b);
-    const int32_t* trow = A.table + (long long)b * A.max_blocks;
-    const long long k_off = ((long long)(A.layer * 2) * A.Hkv + h) * kBT * D;
-    const long long v_off = ((long long)(A.layer * 2 + 1) * A.Hkv + h) * kBT * D;
-    for (int p = cur - seq0 + warp + 4 * lane; p < pe - seq0; p += 128) {
-      const int blk = p * kBT < ctx_b ? __ldg(trow + p) : -1;
-      if (blk >= 0) {
-        const bf16* page = A.pool + (long long)blk * A.block_el;
-        l2_prefetch_bulk(page + k_off, kBT * D * 2);
-        l2_prefetch_bulk(page + v_off, kBT * D * 2);
-      }
-    }
-    cur = pe;
-  }
-  __shared__ int s_attn_last;
-  constexpr int EPT = (G * D + kEpiThreads - 1) / kEpiThreads;   // merged elements per thread
-  unsigned heads_ready = 0;
-  for (int cur = my0; cur < my1;) {
-    int b, h, seq0, seq1, pe;
-    resolve(cur, b, h, seq0, seq1, pe);
-    const int pa = cur - seq0, pb = pe - seq0;
-    const bool first_piece = cur == my0;
-    if (!(heads_ready >> h & 1)) {
-      attn_wait_qkv(A, h, epoch, lane);
-      heads_ready |= 1u << h;
-    }
-    mark(1, first_piece);
-    const int ctx_b = __ldg(A.ctx + b);
-    const int r8 = lane >> 2, quad = lane & 3;
-    uint32_t qa[D / 8];
-    attn_load_q<D>(A.q + (long long)b * A.q_stride + (long long)(h * G + r8) * D, r8 < G, quad, qa);
-    mark(2, first_piece);
-    AttnAcc<D> st;
-    const PageSrc src = page_src<D>(A.pool, A.block_el, A.layer, A.Hkv, h, A.table + (long long)b * A.max_blocks,
-                                    A.scale_log2);
-    attn_pages<D>(src, pa + warp, pb, 4, ctx_b, qa, vs, st, lane, (atr && first_piece) ? atr + 8 : nullptr);
-    mark(3, first_piece);
-    // ---- CTA merge of the 4 warps' states (warp order) through shared memory
-    float* wst = reinterpret_cast<float*>(vs);   // this warp's V page is free now: [G] m, [G] l, [G][D] o
-    __syncwarp();
-    if (r8 < G) {
-#pragma unroll
-      for (int n = 0; n < D / 8; ++n)
-        *reinterpret_cast<float2*>(wst + 2 * G + r8 * D + 8 * n + 2 * quad) = make_float2(st.o[n][0], st.o[n][1]);
-      if (quad == 0) {
-        wst[r8] = st.m;
-        wst[G + r8] = st.l;
-      }
-    }
+__device__ __noinline__ void attn_phase(const MkPhase& P, int pidx, int epoch, int cta, int grid, int warp, int lane,
+                                        bf16* vs_all, int* out_flags, unsigned long long* atr) {
+  const AttnDesc& D_ = P.attn;
+  AttnWork A;
+  A.pool = D_.pool;
+  A.block_el = D_.block_el;
+  A.layer = D_.layer;
+  A.Hq = D_.Hq;
+  A.Hkv = D_.Hkv;
+  A.q = D_.q;
+  A.q_stride = D_.q_stride;
+  A.table = D_.table;
+  A.max_blocks = D_.max_blocks;
+  A.ctx = D_.ctx;
+  A.out = D_.out;
+  A.scale_log2 = D_.scale_log2;
+  A.ws = D_.ws;
+  A.tag = ((unsigned)epoch << 8) | (unsigned)(pidx & 255);
+  A.prefetch = 1;
+  A.min_pages = D_.min_pages;
+  A.M = P.M;
+  auto wait_head = [&](int h, int ln) { attn_wait_qkv(D_, h, epoch, ln); };
+  auto done_head = [&](int h, int et) {
+    // publish: the O projection reads att through TMA (async proxy)
+    fence_proxy_async_all();
     epi_bar();
-    float Mv[EPT], Lv[EPT], Ov[EPT];
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      const int idx = et * EPT + e, g = idx / D, dd = idx % D;
-      Mv[e] = -INFINITY;
-      Lv[e] = 0.f;
-      Ov[e] = 0.f;
-      if (idx < G * D) {
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const float* ws = reinterpret_cast<const float*>(vs_all + w * (kAttnSmem / 2));
-          const float mk = ws[g], mn = fmaxf(Mv[e], mk);
-          const float a0 = mn == -INFINITY ? 0.f : exp2f(Mv[e] - mn), a1 = mn == -INFINITY ? 0.f : exp2f(mk - mn);
-          Lv[e] = Lv[e] * a0 + ws[G + g] * a1;
-          Ov[e] = Ov[e] * a0 + ws[2 * G + g * D + dd] * a1;
-          Mv[e] = mn;
-        }
+    if (et == 0) {
+      if (atom_add_acq_rel(D_.head_ctr + h, 1) == P.M - 1) {
+        D_.head_ctr[h] = 0;
+        set_flag(out_flags, h, epoch);
       }
     }
-    const int first_c = seq0 / qc, last_c = (seq1 - 1) / qc;
-    const int nparts = last_c - first_c + 1;
-    bool done = nparts == 1;
-    if (!done) {
-      // CTA partial (layout m[G], l[G], o[G][D]); slot 0: the CTA's first piece
-      float* part = A.ws + ((long long)cta * 2 + (first_piece ? 0 : 1)) * G * (D + 2);
-#pragma unroll
-      for (int e = 0; e < EPT; ++e) {
-        const int idx = et * EPT + e, g = idx / D, dd = idx % D;
-        if (idx < G * D) {
-          __stcg(part + 2 * G + idx, Ov[e]);
-          if (dd == 0) {
-            __stcg(part + g, Mv[e]);
-            __stcg(part + G + g, Lv[e]);
-          }
-        }
-      }
-      // publish the partial: one release/acquire RMW for the CTA after the
-      // barrier (cumulativity), as in the GEMM fix-up
-      epi_bar();
-      int* ctr = A.seq_ctr + b * Hkv + h;
-      if (et == 0) s_attn_last = atom_add_acq_rel(ctr, 1) == nparts - 1;
-      epi_bar();
-      mark(4, first_piece);
-      if (s_attn_last) {
-#pragma unroll
-        for (int e = 0; e < EPT; ++e) {
-          Mv[e] = -INFINITY;
-          Lv[e] = 0.f;
-          Ov[e] = 0.f;
-        }
-        for (int c0 = first_c; c0 <= last_c; c0 += 8) {
-          float pm[8][EPT], pl[8][EPT], po[8][EPT];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int c = c0 + k;
-            const float* pp = A.ws + ((long long)c * 2 + ((c == first_c && c * qc < seq0) ? 1 : 0)) * G * (D + 2);
-#pragma unroll
-            for (int e = 0; e < EPT; ++e) {
-              const int idx = et * EPT + e, g = idx / D;
-              const bool ok = c <= last_c && idx < G * D;
-              pm[k][e] = ok ? __ldcg(pp + g) : -INFINITY;
-              pl[k][e] = ok ? __ldcg(pp + G + g) : 0.f;
-              po[k][e] = ok ? __ldcg(pp + 2 * G + idx) : 0.f;
-            }
-          }
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-#pragma unroll
-            for (int e = 0; e < EPT; ++e) {
-              const float mn = fmaxf(Mv[e], pm[k][e]);
-              const float a0 = mn == -INFINITY ? 0.f : exp2f(Mv[e] - mn);
-              const float a1 = mn == -INFINITY ? 0.f : exp2f(pm[k][e] - mn);
-              Lv[e] = Lv[e] * a0 + pl[k][e] * a1;
-              Ov[e] = Ov[e] * a0 + po[k][e] * a1;
-              Mv[e] = mn;
-            }
-          }
-        }
-        if (et == 0) *ctr = 0;
-        done = true;
-        mark(5, first_piece);
-      }
-    }
-    if (done) {
-      bf16* out = A.out + (long long)b * (A.Hq * D) + (long long)h * G * D;
-#pragma unroll
-      for (int e = 0; e < EPT; ++e) {
-        const int idx = et * EPT + e;
-        if (idx < G * D) out[idx] = f2bf(Lv[e] > 0.f ? Ov[e] / Lv[e] : 0.f);
-      }
-      // publish: the O projection reads att through TMA (async proxy)
-      fence_proxy_async_all();
-      epi_bar();
-      if (et == 0) {
-        if (atom_add_acq_rel(A.head_ctr + h, 1) == M - 1) {
-          A.head_ctr[h] = 0;
-          set_flag(out_flags, h, epoch);
-        }
-      }
-    }
-    mark(6, first_piece);
-    epi_bar();   // the warps' shared-memory states are rewritten by the next piece
-    cur = pe;
-  }
-  mark(7, true);
+  };
+  attn_cta_phase<D, G>(A, cta, grid, warp, lane, vs_all, wait_head, done_head, atr);
 }
 
-__device__ void attn_dispatch(const MkPhase& P, int epoch, int cta, int grid, int warp, int lane, bf16* vs,
+__device__ void attn_dispatch(const MkPhase& P, int pidx, int epoch, int cta, int grid, int warp, int lane, bf16* vs,
                               unsigned long long* atr) {
   const int D = P.attn.D, G = P.attn.G;
-  if (D == 128 && G == 4) attn_phase<128, 4>(P, epoch, cta, grid, warp, lane, vs, P.out_flags, atr);
+  if (D == 128 && G == 4) attn_phase<128, 4>(P, pidx, epoch, cta, grid, warp, lane, vs, P.out_flags, atr);
 #ifndef MK_ONLY_8B
-  else if (D == 64 && G == 2) attn_phase<64, 2>(P, epoch, cta, grid, warp, lane, vs, P.out_flags, atr);
-  else if (D == 64 && G == 4) attn_phase<64, 4>(P, epoch, cta, grid, warp, lane, vs, P.out_flags, atr);
+  else if (D == 64 && G == 2) attn_phase<64, 2>(P, pidx, epoch, cta, grid, warp, lane, vs, P.out_flags, atr);
+  else if (D == 64 && G == 4) attn_phase<64, 4>(P, pidx, epoch, cta, grid, warp, lane, vs, P.out_flags, atr);
 #endif
 }
 
@@ -469,7 +285,7 @@ __global__ void __launch_bounds__(kMkThreads, 1)
   float* red = reinterpret_cast<float*>(xch + BN * kBM);      // [4][BN]
   float* rs = red + 4 * BN;                                   // [BN]
   bf16* vs_all = reinterpret_cast<bf16*>(
-      (reinterpret_cast<uintptr_t>(rs + BN) + 127) & ~uintptr_t(127));   // [4][16][D] V pages (attention)
+      (reinterpret_cast<uintptr_t>(rs + BN) + 127) & ~uintptr_t(127));   // [4][kAttnWarpBytes] (attention)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x, grid = gridDim.x;
@@ -624,7 +440,7 @@ __global__ void __launch_bounds__(kMkThreads, 1)
     for (int p = 0; p < nph; ++p) {
       const MkPhase& P = prog[p];
       if (P.kind == PK_ATTN) {
-        attn_dispatch(P, epoch, cta, grid, ew, lane, vs_all,
+        attn_dispatch(P, p, epoch, cta, grid, ew, lane, vs_all,
                       (trace && p == 1) ? trace + (long long)grid * nph * 8 + grid + (cta * 4 + ew) * 16 : nullptr);
         epi_bar();
         if (et == 0) stamp(p, 2);
@@ -950,9 +766,8 @@ extern "C" int astraea_step_program_build(int32_t M, int32_t nph, const astraea_
       A.out = (bf16*)q.out_dev;
       A.scale_log2 = q.scale * 1.4426950408889634f;
       A.qkv_flags = flags_of(q.qkv_from);
-      A.seq_ctr = (int*)(ws + L.attn_seq);
       A.head_ctr = (int*)(ws + L.attn_head);
-      A.ws = (float*)(ws + L.attn_ws);
+      A.ws = (unsigned long long*)(ws + L.attn_ws);
       static int min_pages = [] {
         const char* e = getenv("ASTRAEA_ATTN_MIN_PAGES");
         return e ? std::max(1, atoi(e)) : 1;

@@ -42,6 +42,7 @@
 
 #include "common.cuh"
 #include "tc.cuh"
+#include "attn_mma.cuh"
 
 
 using namespace astraea;
@@ -599,8 +600,12 @@ struct ChainArgs {
   int* phase_ctr;              // [kMaxPhases + 1] phase / kernel arrival counters, zero between launches
   int M, grid, nph;
   int l2_pre;                  // weight tiles per CTA prefetched into L2 before griddepcontrol.wait
+  int attn;                    // attention variant run before phase 0 (0: none; 1: D128 G4; 2: D64 G2; 3: D64 G4)
+  attn::AttnWork at;           // its output is phase 0's A
+  int pf_layer;                // >= 0: prefetch that layer's K/V pages into L2 during the last phase
   SkPhase ph[kMaxPhases];
 };
+constexpr int kAttnCtr = kMaxPhases + 2;   // phase_ctr slot: CTAs done with the attention phase
 
 
 __device__ __forceinline__ int sk_owner(long long u, long long units, int grid) {
@@ -630,11 +635,13 @@ __global__ void __launch_bounds__(kThreads, MINB)
   bf16* xch = reinterpret_cast<bf16*>(tmem_slot + 4);        // [BN][128]
   float* red = reinterpret_cast<float*>(xch + BN * kBM);     // [4][BN]
   float* rs = red + 4 * BN;                                  // [BN]
+  constexpr bool kAttn = MINB == 1;                          // deep (layer) chains carry the attention phase
+  bf16* vs_all = reinterpret_cast<bf16*>((reinterpret_cast<uintptr_t>(rs + BN) + 127) & ~uintptr_t(127));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
   const int G = args.grid;
-  unsigned long long* tr = args.trace ? args.trace + (long long)cta * 16 : nullptr;
+  unsigned long long* tr = args.trace ? args.trace + (long long)cta * 32 : nullptr;   // [0..15] phases, [16..31] attention
   if (tr && threadIdx.x == 0) tr[0] = gtimer();
 
   if (warp == 0 && lane == 0) {
@@ -676,7 +683,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
           mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
           tma_load_2d(sa + s * A_BYTES, &maps.w[p], &full[s], (int)(u % KB) * kBK, (int)(u / KB) * kBM);
         }
-        if (p == 0) {
+        if (p == 0 && kAttn && args.attn) {
+          pdl_wait();
+          wait_phase(args.phase_ctr + kAttnCtr, G);   // every CTA's share of the attention is written
+          asm volatile("fence.proxy.async;" ::: "memory");
+        } else if (p == 0) {
           // While the previous kernel (the layer's attention) finishes, keep
           // HBM busy: prefetch the next l2_pre weight tiles of this CTA's
           // stream (beyond the smem ring) into L2.
@@ -759,6 +770,28 @@ __global__ void __launch_bounds__(kThreads, MINB)
   } else {
     pdl_wait();
     const int epoch = __ldcg(args.phase_ctr + kMaxPhases + 1) + 1;   // launches completed on this workspace + 1
+    if constexpr (kAttn) {
+      if (args.attn) {
+        // The layer's paged decode attention (attn_mma.cuh), by this CTA's
+        // epilogue warps, while warp 0 already streams the O projection's
+        // weight tiles into the ring; its output becomes phase 0's A.
+        const int ew = warp - 2;
+        auto no_wait = [](int, int) {};
+        auto done = [](int, int) { asm volatile("fence.proxy.async;" ::: "memory"); };
+        attn::AttnWork aw = args.at;
+        aw.tag = ((unsigned)epoch << 3) | 6u;
+        unsigned long long* atr = (tr && ew == 0) ? tr + 16 : nullptr;
+        if (args.attn == 1) attn::attn_cta_phase<128, 4>(aw, cta, G, ew, lane, vs_all, no_wait, done, atr);
+        else if (args.attn == 2) attn::attn_cta_phase<64, 2>(aw, cta, G, ew, lane, vs_all, no_wait, done);
+        else attn::attn_cta_phase<64, 4>(aw, cta, G, ew, lane, vs_all, no_wait, done);
+        asm volatile("fence.proxy.async;" ::: "memory");
+        epi_bar();
+        if (threadIdx.x == 64) {
+          atom_add_acq_rel(args.phase_ctr + kAttnCtr, 1);
+          if (tr) tr[15] = gtimer();   // this CTA's attention share written
+        }
+      }
+    }
     const int quarter = warp & 3;
     const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
     const int row = quarter * 32 + lane;  // feature within the tile
@@ -779,6 +812,15 @@ __global__ void __launch_bounds__(kThreads, MINB)
       if (P.epi.ssq_in) {
         if (row < args.M) rs[row] = rms_scale(P.epi, args.M, row);
         epi_bar();
+      }
+      if constexpr (kAttn) {
+        if (args.attn && args.pf_layer >= 0 && p == args.nph - 1) {
+          // the next layer's attention (next launch) reads these pages: warm L2 now
+          attn::AttnWork nx = args.at;
+          nx.layer = args.pf_layer;
+          if (args.attn == 1) attn::attn_cta_prefetch<128>(nx, cta, G, warp - 2, lane);
+          else attn::attn_cta_prefetch<64>(nx, cta, G, warp - 2, lane);
+        }
       }
       // Split tiles are finished by c_first, the CTA owning the tile's first
       // k-blocks: its segment closes its range while the others open theirs,
@@ -876,6 +918,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     // the last CTA to leave resets the phase counters for the next launch
     if (atom_add_acq_rel(args.phase_ctr + kMaxPhases, 1) == G - 1) {
       for (int p = 0; p <= kMaxPhases; ++p) args.phase_ctr[p] = 0;
+      args.phase_ctr[kAttnCtr] = 0;
       args.phase_ctr[kMaxPhases + 1] += 1;   // launch epoch (tags of the stream-K partials)
     }
     if (tr) tr[10] = gtimer();
@@ -971,19 +1014,23 @@ SkPlan sk_plan(int M, int N, int K) {
 // fp32 partials of split tiles.
 constexpr size_t kCounterBytes = 16384 * sizeof(int);
 constexpr size_t kPhaseBytes = 256;
+// attention phase of a layer chain: [grid <= 192][G <= 4][D + 2 <= 130] tagged split partials
+constexpr size_t kAttnWsBytes = (size_t)192 * 4 * 130 * sizeof(unsigned long long);
+constexpr size_t kHeadBytes = kCounterBytes + kPhaseBytes + kAttnWsBytes;   // before the GEMM partials
 
 size_t partial_bytes(int M, const SkPlan& p) { return (size_t)p.tiles * p.maxseg * M * kBM * sizeof(unsigned long long); }
 
-template <int BN>
+template <int BN, bool DEEP = false>
 constexpr size_t sk_extra_bytes() {
-  return (size_t)BN * kBM * 2 + 5 * BN * sizeof(float) + 64;
+  // DEEP (layer) chains also hold the attention phase's four V pages
+  return (size_t)BN * kBM * 2 + 5 * BN * sizeof(float) + 64 + (DEEP ? 128 + 4 * (size_t)attn::kAttnWarpBytes : 0);
 }
 // Single GEMMs: ~104 KB so two CTAs fit per SM and the next kernel's CTA can
 // become resident and prefetch its weights (PDL) while this one drains.
 // Chains: one deep ring per SM (~200 KB), the phases hide each other's tails.
 template <int BN, bool DEEP>
 constexpr int sk_stages() {
-  return (int)(((DEEP ? 200 : 104) * 1024 - sk_extra_bytes<BN>()) / (kBM * kBK * 2 + BN * kBK * 2));
+  return (int)(((DEEP ? 200 : 104) * 1024 - sk_extra_bytes<BN, DEEP>()) / (kBM * kBK * 2 + BN * kBK * 2));
 }
 
 template <int BN, bool DEEP>
@@ -991,7 +1038,7 @@ int launch_chain(const ChainMaps& maps, const ChainArgs& a, cudaStream_t st) {
   constexpr int S = sk_stages<BN, DEEP>();
   auto kern = gemm_chain_kernel<BN, S, DEEP ? 1 : 2>;
   constexpr size_t smem = 1024 + (size_t)S * (kBM * kBK * 2 + BN * kBK * 2) + (2 * S + 4) * 8 + 16 +
-                          sk_extra_bytes<BN>();
+                          sk_extra_bytes<BN, DEEP>();
   static bool attr = false;
   if (!attr) {
     ASTRAEA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1133,7 +1180,7 @@ extern "C" int astraea_rope_table(const int32_t* positions, int32_t T, int32_t h
 static size_t chain_ws_bytes(int M, int nph, const astraea_gemm_phase* ph) {
   size_t part = 0;
   for (int p = 0; p < nph; ++p) part = std::max(part, partial_bytes(M, sk_plan(M, ph[p].N, ph[p].K)));
-  return kCounterBytes + kPhaseBytes + part;
+  return kHeadBytes + part;
 }
 
 // K-splits of the CTA-pair GEMM: only when its tiles leave pairs idle (small
@@ -1164,9 +1211,9 @@ extern "C" size_t astraea_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K) 
   if (M <= 0 || N <= 0 || K <= 0) return 0;
   if (M > kColsMaxM) {
     const size_t p = pair_partial_bytes(M, N, K);
-    return p ? kCounterBytes + kPhaseBytes + p : 0;
+    return p ? kHeadBytes + p : 0;
   }
-  return kCounterBytes + kPhaseBytes + partial_bytes(M, sk_plan(M, N, K));
+  return kHeadBytes + partial_bytes(M, sk_plan(M, N, K));
 }
 
 extern "C" size_t astraea_gemm_chain_workspace_bytes(int32_t M, int32_t nphases, const astraea_gemm_phase* phases) {
@@ -1176,7 +1223,7 @@ extern "C" size_t astraea_gemm_chain_workspace_bytes(int32_t M, int32_t nphases,
 
 // Build and launch a chain of 1..kMaxPhases decode GEMMs (M <= 64 tokens).
 static int run_chain(int M, int nph, const astraea_gemm_phase* ph, void* ws, size_t ws_bytes, bool deep,
-                     cudaStream_t st) {
+                     cudaStream_t st, const astraea_attn_phase* at = nullptr) {
   if (M <= 0 || M > kColsMaxM || nph <= 0 || nph > kMaxPhases) return ASTRAEA_EINVAL;
   if (!ws || ws_bytes < chain_ws_bytes(M, nph, ph)) return ASTRAEA_EINVAL;
   ChainMaps maps;
@@ -1188,7 +1235,47 @@ static int run_chain(int M, int nph, const astraea_gemm_phase* ph, void* ws, siz
   }
   a.counters = (int*)ws;
   a.phase_ctr = (int*)((char*)ws + kCounterBytes);
-  a.ws = (float*)((char*)ws + kCounterBytes + kPhaseBytes);
+  a.ws = (float*)((char*)ws + kHeadBytes);
+  a.attn = 0;
+  a.pf_layer = -1;
+  if (at) {
+    const astraea_kv_geometry& g = at->geo;
+    if (!deep || !at->pool_dev || !at->q_dev || !at->table_dev || !at->ctx_dev || !at->out_dev ||
+        g.block_tokens != 16 || g.num_kv_heads <= 0 || g.num_kv_heads > 32 || at->num_q_heads % g.num_kv_heads ||
+        at->layer < 0 || at->layer >= g.num_layers || at->max_blocks <= 0)
+      return ASTRAEA_EINVAL;
+    const int G = at->num_q_heads / g.num_kv_heads, D = g.head_dim;
+    a.attn = (D == 128 && G == 4) ? 1 : (D == 64 && G == 2) ? 2 : (D == 64 && G == 4) ? 3 : 0;
+    if (!a.attn || num_sms() > 192) return ASTRAEA_EUNSUPPORTED;
+    attn::AttnWork& w = a.at;
+    w.pool = (const bf16*)at->pool_dev;
+    w.block_el = (long long)astraea_kv_block_bytes(&g) / 2;
+    w.layer = at->layer;
+    w.Hq = at->num_q_heads;
+    w.Hkv = g.num_kv_heads;
+    w.q = (const bf16*)at->q_dev;
+    w.q_stride = at->q_row_stride;
+    w.table = at->table_dev;
+    w.max_blocks = at->max_blocks;
+    w.ctx = at->ctx_dev;
+    w.out = (bf16*)at->out_dev;
+    w.scale_log2 = at->scale * 1.4426950408889634f;
+    w.ws = (unsigned long long*)((char*)ws + kCounterBytes + kPhaseBytes);
+    w.tag = 0;   // set on the device from the launch epoch
+    w.prefetch = 0;   // no wait before the page loads: nothing to overlap
+    static const int min_pages = [] {
+      const char* e = getenv("ASTRAEA_CHAIN_ATTN_MIN_PAGES");
+      return e ? std::max(1, atoi(e)) : 2;   // pages per warp: measured best at batch 1-16
+    }();
+    w.min_pages = min_pages;
+    static const bool pf = [] {
+      const char* e = getenv("ASTRAEA_CHAIN_KV_PREFETCH");
+      return e && e[0] == '1';   // measured neutral at batch 1, -3% at batch 16: off
+    }();
+    a.pf_layer = (pf && at->layer + 1 < g.num_layers) ? at->layer + 1 : -1;
+    w.M = M;
+    if (ph[0].A != at->out_dev) return ASTRAEA_EINVAL;   // the attention output is phase 0's input
+  }
   a.M = M;
   a.grid = num_sms();
   a.nph = nph;
@@ -1240,6 +1327,12 @@ extern "C" int astraea_gemm_chain(int32_t M, int32_t nphases, const astraea_gemm
   return run_chain(M, nphases, phases, ws, ws_bytes, true, (cudaStream_t)stream);
 }
 
+extern "C" int astraea_gemm_chain_attn(int32_t M, const astraea_attn_phase* attn, int32_t nphases,
+                                       const astraea_gemm_phase* phases, void* ws, size_t ws_bytes, void* stream) {
+  if (!phases || !attn) return ASTRAEA_EINVAL;
+  return run_chain(M, nphases, phases, ws, ws_bytes, true, (cudaStream_t)stream, attn);
+}
+
 extern "C" int astraea_gemm_bf16_ex(const void* A, int32_t lda, const void* W, int32_t ldw, void* C, int32_t ldc,
                                     int32_t M, int32_t N, int32_t K, const astraea_epilogue* epi, void* ws,
                                     size_t ws_bytes, void* stream) {
@@ -1281,9 +1374,9 @@ extern "C" int astraea_gemm_bf16_ex(const void* A, int32_t lda, const void* W, i
     a.part = nullptr;
     a.ctr = nullptr;
     if (a.splits > 1) {
-      if (ws && ws_bytes >= kCounterBytes + kPhaseBytes + pair_partial_bytes(M, N, K)) {
+      if (ws && ws_bytes >= kHeadBytes + pair_partial_bytes(M, N, K)) {
         a.ctr = (int*)((char*)ws + kCounterBytes);
-        a.part = (unsigned long long*)((char*)ws + kCounterBytes + kPhaseBytes);
+        a.part = (unsigned long long*)((char*)ws + kHeadBytes);
       } else {
         a.splits = 1;   // no workspace: unsplit (fewer pairs busy, same result)
       }

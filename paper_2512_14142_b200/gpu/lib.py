@@ -80,6 +80,24 @@ PHASE_GEMM = 0
 PHASE_ATTN = 1
 
 
+class AttnPhase(ctypes.Structure):
+    """astraea_attn_phase (include/astraea_b200.h)."""
+
+    _fields_ = [
+        ("pool_dev", ctypes.c_void_p),
+        ("geo", KvGeometry),
+        ("layer", ctypes.c_int32),
+        ("num_q_heads", ctypes.c_int32),
+        ("q_dev", ctypes.c_void_p),
+        ("q_row_stride", ctypes.c_int32),
+        ("table_dev", ctypes.c_void_p),
+        ("max_blocks", ctypes.c_int32),
+        ("ctx_dev", ctypes.c_void_p),
+        ("scale", ctypes.c_float),
+        ("out_dev", ctypes.c_void_p),
+    ]
+
+
 class StepPhase(ctypes.Structure):
     """astraea_step_phase (include/astraea_b200.h)."""
 
@@ -139,6 +157,8 @@ SIGNATURES = {
     "astraea_rope_table": (ctypes.c_int, [_vp, _i32, _i32, _f32, _vp, _vp]),
     "astraea_gemm_chain_workspace_bytes": (_sz, [_i32, _i32, ctypes.POINTER(GemmPhase)]),
     "astraea_gemm_chain": (ctypes.c_int, [_i32, _i32, ctypes.POINTER(GemmPhase), _vp, _sz, _vp]),
+    "astraea_gemm_chain_attn": (
+        ctypes.c_int, [_i32, ctypes.POINTER(AttnPhase), _i32, ctypes.POINTER(GemmPhase), _vp, _sz, _vp]),
     "astraea_step_program_bytes": (_sz, [_i32]),
     "astraea_step_workspace_bytes": (_sz, [_i32, _i32, ctypes.POINTER(StepPhase)]),
     "astraea_step_program_build": (ctypes.c_int, [_i32, _i32, ctypes.POINTER(StepPhase), _vp, _sz, _vp, _sz]),

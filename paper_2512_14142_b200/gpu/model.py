@@ -220,6 +220,9 @@ class LlamaRunner:
         # default: on B200 it matches the per-layer chain at batch 1 and trails
         # it at larger batches ("decode-step kernel")
         self.use_step_kernel = False
+        # the layer's decode attention runs inside its chained-GEMM launch
+        # (astraea_gemm_chain_attn) instead of as a separate kernel
+        self.fuse_attention = True
         self.l2_ahead = 0
         self._mk = None
         self._programs: dict = {}
@@ -308,9 +311,10 @@ class LlamaRunner:
         ``keys_out`` the sampled tokens stay on the device as argmax keys.
 
         Launches: embedding, RoPE table, layer 0's QKV GEMM, then per layer
-        the paged attention and ONE chained GEMM kernel running O-proj ->
-        gate/up -> down -> next layer's QKV (the last layer's chain ends
-        with lm_head + argmax instead) -- 2 launches per layer."""
+        ONE kernel running the paged attention and the chained GEMMs O-proj
+        -> gate/up -> down -> next layer's QKV (the last layer's chain ends
+        with lm_head + argmax instead); with fuse_attention off the
+        attention is a separate launch (2 per layer)."""
         if self.cfg.num_layers < 1 or tokens.shape[0] > 64:
             return self._decode_unchained(tokens, positions, slots, table, ctx, stream, want_logits, keys_out)
         if self.use_step_kernel and self._step_supported():
@@ -341,9 +345,11 @@ class LlamaRunner:
                         positions=positions, slots=slots, rope_theta=cfg.rope_theta, rope_table=cs)
 
         ops.gemm_ex(**qkv(0, ssq0), workspace=ws, stream=stream)
+        fuse = self.fuse_attention and self._attn_fusable()
         for li, lw in enumerate(w.layers):
-            ops.decode_attention(pool.geo, pool.data, li, q, qd, B, cfg.num_q_heads, table, ctx, self.scale,
-                                 att, dws, stream=stream)
+            if not fuse:
+                ops.decode_attention(pool.geo, pool.data, li, q, qd, B, cfg.num_q_heads, table, ctx, self.scale,
+                                     att, dws, stream=stream)
             phases = [
                 dict(a=att, w=lw["wo"], out=x, kind=L.EPI_RESIDUAL, residual=x, ssq_out=ssq_mid),
                 dict(a=x, w=lw["wgu"], out=h, kind=L.EPI_SILU, ssq_in=ssq_mid, rms_dim=d, rms_eps=eps),
@@ -354,10 +360,17 @@ class LlamaRunner:
             else:
                 phases.append(dict(a=x, w=w.lm_head, out=None, kind=L.EPI_ARGMAX, ssq_in=ssq, rms_dim=d, rms_eps=eps,
                                    argmax_keys=keys))
-            ops.gemm_chain(phases, ws, stream=stream)
+            attn = (dict(pool=pool.data, geo=pool.geo, layer=li, num_q_heads=cfg.num_q_heads, q=q, q_stride=qd,
+                         table=table, ctx=ctx, scale=self.scale, out=att) if fuse else None)
+            ops.gemm_chain(phases, ws, stream=stream, attn=attn)
         if keys_out is not None:
             return keys_out
         return ops.keys_to_ids(keys)
+
+    def _attn_fusable(self) -> bool:
+        cfg = self.cfg
+        G = cfg.num_q_heads // cfg.num_kv_heads
+        return (cfg.head_dim, G) in ((128, 4), (64, 2), (64, 4))
 
     def _step_supported(self) -> bool:
         cfg = self.cfg

@@ -81,11 +81,14 @@ def _epilogue(kind=L.EPI_NONE, residual=None, ssq_out=None, ssq_in=None, rms_dim
     return e
 
 
-def gemm_chain(phases, workspace, stream=None):
+def gemm_chain(phases, workspace, stream=None, attn=None):
     """Dependent decode GEMMs in one persistent launch (astraea_gemm_chain).
 
     ``phases``: list of dicts with a, w, out and the ``gemm_ex`` epilogue
-    keywords; every ``a`` has the same number of rows (M <= 64)."""
+    keywords; every ``a`` has the same number of rows (M <= 64). ``attn``
+    (optional dict: pool, geo, layer, num_q_heads, q, q_stride, table, ctx,
+    scale, out): the layer's decode attention runs first in the same launch
+    (astraea_gemm_chain_attn); its ``out`` must be phase 0's ``a``."""
     lib = L.require_cuda()
     n = len(phases)
     arr = (L.GemmPhase * n)()
@@ -101,8 +104,18 @@ def gemm_chain(phases, workspace, stream=None):
         q.epi = _epilogue(**{k: v for k, v in ph.items() if k not in ("a", "w", "out")})
     need = lib.astraea_gemm_chain_workspace_bytes(M, n, arr)
     assert workspace.numel() * workspace.element_size() >= need, "chain workspace too small"
-    L.check(lib.astraea_gemm_chain(M, n, arr, L.ptr(workspace), workspace.numel() * workspace.element_size(),
-                                   _s(stream)), "gemm_chain")
+    if attn is None:
+        L.check(lib.astraea_gemm_chain(M, n, arr, L.ptr(workspace), workspace.numel() * workspace.element_size(),
+                                       _s(stream)), "gemm_chain")
+    else:
+        at = L.AttnPhase()
+        at.pool_dev, at.geo, at.layer = L.ptr(attn["pool"]), attn["geo"], attn["layer"]
+        at.num_q_heads, at.q_dev, at.q_row_stride = attn["num_q_heads"], L.ptr(attn["q"]), attn["q_stride"]
+        at.table_dev, at.max_blocks = L.ptr(attn["table"]), attn["table"].shape[1]
+        at.ctx_dev, at.scale, at.out_dev = L.ptr(attn["ctx"]), attn["scale"], L.ptr(attn["out"])
+        L.check(lib.astraea_gemm_chain_attn(M, ctypes.byref(at), n, arr, L.ptr(workspace),
+                                            workspace.numel() * workspace.element_size(), _s(stream)),
+                "gemm_chain_attn")
     _count()
 
 

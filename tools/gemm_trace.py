@@ -45,13 +45,13 @@ for _ in range(3):
 torch.cuda.synchronize()
 reps = 3
 lib = L.load()
-buf = torch.zeros(reps, 148 * 16, dtype=torch.int64, device=dev)
-lib.astraea_debug_gemm_trace(buf.data_ptr(), reps, 148 * 16)
+buf = torch.zeros(reps, 148 * 32, dtype=torch.int64, device=dev)
+lib.astraea_debug_gemm_trace(buf.data_ptr(), reps, 148 * 32)
 for _ in range(reps):
     ops.gemm_chain(phases, ws)
 torch.cuda.synchronize()
 lib.astraea_debug_gemm_trace(None, 0, 0)
-t = buf.view(reps, 148, 16).cpu().double()
+t = buf.view(reps, 148, 32).cpu().double()
 names = ["o", "gu", "down", "qkv"]
 
 

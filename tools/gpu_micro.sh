@@ -1,5 +1,8 @@
 rm -f gpurun_out/micro.log
-timeout 600 python -m pytest tests/test_gpu_step.py -x -q 2>&1 | grep -E "Error|assert|passed|failed" | head -20 >> gpurun_out/micro.log
-timeout 300 python tools/step_micro.py 1 16 2>&1 | grep -v slowest >> gpurun_out/micro.log
-timeout 300 python tools/step_timing.py --batch 1 4 16 --l2 0 >> gpurun_out/micro.log 2>&1
+for v in "0 1" "0 2"; do
+set -- $v
+echo "kvprefetch=$1 minpages=$2" >> gpurun_out/micro.log
+ASTRAEA_CHAIN_KV_PREFETCH=$1 ASTRAEA_CHAIN_ATTN_MIN_PAGES=$2 timeout 300 python tools/step_timing.py --batch 1 4 16 --l2 0 2>&1 | grep layers >> gpurun_out/micro.log
+done
+ASTRAEA_CHAIN_KV_PREFETCH=0 timeout 300 python tools/chain_trace.py --layers 16 >> gpurun_out/micro.log 2>&1
 cat gpurun_out/micro.log
