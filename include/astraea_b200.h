@@ -276,9 +276,12 @@ typedef struct {
   float scale;
   void* out_dev;
 } astraea_attn_phase;
-ASTRAEA_API int astraea_gemm_chain_attn(int32_t M, const astraea_attn_phase* attn, int32_t nphases,
-                           const astraea_gemm_phase* phases, void* workspace_dev, size_t workspace_bytes,
-                           void* stream);
+/* attn[k] runs right before GEMM phase attn_before[k] (strictly increasing;
+ * attn[k].out_dev must be that phase's A): nattn <= 2, nphases <= 8, so one
+ * launch can carry two whole decoder layers. */
+ASTRAEA_API int astraea_gemm_chain_attn(int32_t M, int32_t nattn, const astraea_attn_phase* attn,
+                           const int32_t* attn_before, int32_t nphases, const astraea_gemm_phase* phases,
+                           void* workspace_dev, size_t workspace_bytes, void* stream);
 ASTRAEA_API int astraea_gemm_bf16_ex(const void* A_dev, int32_t lda, const void* W_dev, int32_t ldw,
                          void* C_dev, int32_t ldc, int32_t M, int32_t N, int32_t K,
                          const astraea_epilogue* epilogue, void* workspace_dev,

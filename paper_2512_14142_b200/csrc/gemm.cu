@@ -51,7 +51,8 @@ using namespace astraea::tc;
 namespace {
 
 constexpr int kThreads = 192;
-constexpr int kMaxPhases = 4;   // GEMMs per chain launch
+constexpr int kMaxPhases = 8;   // GEMMs per chain launch (two layers)
+constexpr int kMaxAttn = 2;     // attention phases per chain launch
 
 struct GemmArgs {
   bf16* C;
@@ -478,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const Epi& e = args.epi;
     const int quarter = warp & 3;
     const uint32_t tempty_leader[2] = {mapa_shared(smem_u32(&tempty[0]), 0), mapa_shared(smem_u32(&tempty[1]), 0)};
-    const unsigned tag = S > 1 ? (((unsigned)__ldcg(args.ctr + kMaxPhases + 1) + 1u) << 3) | 7u : 0u;
+    const unsigned tag = S > 1 ? (((unsigned)__ldcg(args.ctr + kMaxPhases + 1) + 1u) << 4) | 15u : 0u;
     const int row_local = quarter * 32 + lane;
     constexpr long long kPartCta = (long long)HALF * 256;   // words per CTA partial
     int lt = 0;
@@ -600,12 +601,14 @@ struct ChainArgs {
   int* phase_ctr;              // [kMaxPhases + 1] phase / kernel arrival counters, zero between launches
   int M, grid, nph;
   int l2_pre;                  // weight tiles per CTA prefetched into L2 before griddepcontrol.wait
-  int attn;                    // attention variant run before phase 0 (0: none; 1: D128 G4; 2: D64 G2; 3: D64 G4)
-  attn::AttnWork at;           // its output is phase 0's A
+  int nattn;                   // attention phases (layers) in this launch
+  int attn_kind[kMaxAttn];     // 1: D128 G4; 2: D64 G2; 3: D64 G4
+  int attn_before[kMaxAttn];   // the GEMM phase that attention k precedes (its output is that phase's A)
+  attn::AttnWork at[kMaxAttn];
   int pf_layer;                // >= 0: prefetch that layer's K/V pages into L2 during the last phase
   SkPhase ph[kMaxPhases];
 };
-constexpr int kAttnCtr = kMaxPhases + 2;   // phase_ctr slot: CTAs done with the attention phase
+constexpr int kAttnCtr = kMaxPhases + 2;   // phase_ctr slots kAttnCtr + k: CTAs done with attention k
 
 
 __device__ __forceinline__ int sk_owner(long long u, long long units, int grid) {
@@ -683,9 +686,13 @@ __global__ void __launch_bounds__(kThreads, MINB)
           mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
           tma_load_2d(sa + s * A_BYTES, &maps.w[p], &full[s], (int)(u % KB) * kBK, (int)(u / KB) * kBM);
         }
-        if (p == 0 && kAttn && args.attn) {
-          pdl_wait();
-          wait_phase(args.phase_ctr + kAttnCtr, G);   // every CTA's share of the attention is written
+        int ak = -1;
+        if (kAttn)
+          for (int k = 0; k < args.nattn; ++k)
+            if (args.attn_before[k] == p) ak = k;
+        if (ak >= 0) {
+          if (p == 0) pdl_wait();
+          wait_phase(args.phase_ctr + kAttnCtr + ak, G);   // every CTA's share of the attention is written
           asm volatile("fence.proxy.async;" ::: "memory");
         } else if (p == 0) {
           // While the previous kernel (the layer's attention) finishes, keep
@@ -713,7 +720,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
           wait_phase(args.phase_ctr + p - 1, G);
           asm volatile("fence.proxy.async;" ::: "memory");   // generic-proxy writes -> TMA reads
         }
-        if (tr) tr[1 + p] = gtimer();   // activations of phase p released
+        if (tr && p < 4) tr[1 + p] = gtimer();   // activations of phase p released (first layer only)
         for (int k = 0; k < pre; ++k) {
           const int s = (i + k) % STAGES;
           tma_load_2d(sb + s * B_BYTES, &maps.x[p], &full[s], (int)((u0 + k) % KB) * kBK, 0);
@@ -770,28 +777,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
   } else {
     pdl_wait();
     const int epoch = __ldcg(args.phase_ctr + kMaxPhases + 1) + 1;   // launches completed on this workspace + 1
-    if constexpr (kAttn) {
-      if (args.attn) {
-        // The layer's paged decode attention (attn_mma.cuh), by this CTA's
-        // epilogue warps, while warp 0 already streams the O projection's
-        // weight tiles into the ring; its output becomes phase 0's A.
-        const int ew = warp - 2;
-        auto no_wait = [](int, int) {};
-        auto done = [](int, int) { asm volatile("fence.proxy.async;" ::: "memory"); };
-        attn::AttnWork aw = args.at;
-        aw.tag = ((unsigned)epoch << 3) | 6u;
-        unsigned long long* atr = (tr && ew == 0) ? tr + 16 : nullptr;
-        if (args.attn == 1) attn::attn_cta_phase<128, 4>(aw, cta, G, ew, lane, vs_all, no_wait, done, atr);
-        else if (args.attn == 2) attn::attn_cta_phase<64, 2>(aw, cta, G, ew, lane, vs_all, no_wait, done);
-        else attn::attn_cta_phase<64, 4>(aw, cta, G, ew, lane, vs_all, no_wait, done);
-        asm volatile("fence.proxy.async;" ::: "memory");
-        epi_bar();
-        if (threadIdx.x == 64) {
-          atom_add_acq_rel(args.phase_ctr + kAttnCtr, 1);
-          if (tr) tr[15] = gtimer();   // this CTA's attention share written
-        }
-      }
-    }
     const int quarter = warp & 3;
     const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
     const int row = quarter * 32 + lane;  // feature within the tile
@@ -809,16 +794,39 @@ __global__ void __launch_bounds__(kThreads, MINB)
         if (threadIdx.x == 64) wait_phase(args.phase_ctr + p - 1, G);
         epi_bar();
       }
+      if constexpr (kAttn) {
+        for (int k = 0; k < args.nattn; ++k) {
+          if (args.attn_before[k] != p) continue;
+          // A layer's paged decode attention (attn_mma.cuh), by this CTA's
+          // epilogue warps, while warp 0 already streams phase p's weight
+          // tiles into the ring; its output is phase p's A.
+          const int ew = warp - 2;
+          auto no_wait = [](int, int) {};
+          auto done = [](int, int) { asm volatile("fence.proxy.async;" ::: "memory"); };
+          attn::AttnWork aw = args.at[k];
+          aw.tag = ((unsigned)epoch << 4) | (unsigned)(8 + k);
+          unsigned long long* atr = (tr && ew == 0 && k == 0) ? tr + 16 : nullptr;
+          if (args.attn_kind[k] == 1) attn::attn_cta_phase<128, 4>(aw, cta, G, ew, lane, vs_all, no_wait, done, atr);
+          else if (args.attn_kind[k] == 2) attn::attn_cta_phase<64, 2>(aw, cta, G, ew, lane, vs_all, no_wait, done);
+          else attn::attn_cta_phase<64, 4>(aw, cta, G, ew, lane, vs_all, no_wait, done);
+          asm volatile("fence.proxy.async;" ::: "memory");
+          epi_bar();
+          if (threadIdx.x == 64) {
+            atom_add_acq_rel(args.phase_ctr + kAttnCtr + k, 1);
+            if (tr && k == 0) tr[15] = gtimer();   // this CTA's share of attention 0 written
+          }
+        }
+      }
       if (P.epi.ssq_in) {
         if (row < args.M) rs[row] = rms_scale(P.epi, args.M, row);
         epi_bar();
       }
       if constexpr (kAttn) {
-        if (args.attn && args.pf_layer >= 0 && p == args.nph - 1) {
+        if (args.nattn && args.pf_layer >= 0 && p == args.nph - 1) {
           // the next layer's attention (next launch) reads these pages: warm L2 now
-          attn::AttnWork nx = args.at;
+          attn::AttnWork nx = args.at[args.nattn - 1];
           nx.layer = args.pf_layer;
-          if (args.attn == 1) attn::attn_cta_prefetch<128>(nx, cta, G, warp - 2, lane);
+          if (args.attn_kind[0] == 1) attn::attn_cta_prefetch<128>(nx, cta, G, warp - 2, lane);
           else attn::attn_cta_prefetch<64>(nx, cta, G, warp - 2, lane);
         }
       }
@@ -830,7 +838,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
       // spins only on words not yet written -- no arrival counter and no
       // round trip after the last MMA. Sum order: the other segments in CTA
       // order, then the finisher's own (deterministic).
-      const unsigned tag = ((unsigned)epoch << 3) | (unsigned)p;
+      const unsigned tag = ((unsigned)epoch << 4) | (unsigned)p;
       const bool resid = P.epi.kind == EPI_RESIDUAL;
       unsigned long long* wsq = reinterpret_cast<unsigned long long*>(args.ws);
       for (long long u = u0; u < u1; ++seg) {
@@ -907,7 +915,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
       epi_bar();
       if (threadIdx.x == 64) {
         atom_add_acq_rel(args.phase_ctr + p, 1);
-        if (tr) tr[5 + p] = gtimer();
+        if (tr && p < 4) tr[5 + p] = gtimer();
       }
     }
   }
@@ -918,7 +926,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     // the last CTA to leave resets the phase counters for the next launch
     if (atom_add_acq_rel(args.phase_ctr + kMaxPhases, 1) == G - 1) {
       for (int p = 0; p <= kMaxPhases; ++p) args.phase_ctr[p] = 0;
-      args.phase_ctr[kAttnCtr] = 0;
+      for (int k = 0; k < kMaxAttn; ++k) args.phase_ctr[kAttnCtr + k] = 0;
       args.phase_ctr[kMaxPhases + 1] += 1;   // launch epoch (tags of the stream-K partials)
     }
     if (tr) tr[10] = gtimer();
@@ -1223,7 +1231,8 @@ extern "C" size_t astraea_gemm_chain_workspace_bytes(int32_t M, int32_t nphases,
 
 // Build and launch a chain of 1..kMaxPhases decode GEMMs (M <= 64 tokens).
 static int run_chain(int M, int nph, const astraea_gemm_phase* ph, void* ws, size_t ws_bytes, bool deep,
-                     cudaStream_t st, const astraea_attn_phase* at = nullptr) {
+                     cudaStream_t st, int nattn = 0, const astraea_attn_phase* ats = nullptr,
+                     const int32_t* attn_before = nullptr) {
   if (M <= 0 || M > kColsMaxM || nph <= 0 || nph > kMaxPhases) return ASTRAEA_EINVAL;
   if (!ws || ws_bytes < chain_ws_bytes(M, nph, ph)) return ASTRAEA_EINVAL;
   ChainMaps maps;
@@ -1236,18 +1245,22 @@ static int run_chain(int M, int nph, const astraea_gemm_phase* ph, void* ws, siz
   a.counters = (int*)ws;
   a.phase_ctr = (int*)((char*)ws + kCounterBytes);
   a.ws = (float*)((char*)ws + kHeadBytes);
-  a.attn = 0;
+  a.nattn = 0;
   a.pf_layer = -1;
-  if (at) {
+  if (nattn < 0 || nattn > kMaxAttn || (nattn && (!ats || !attn_before || !deep))) return ASTRAEA_EINVAL;
+  for (int k = 0; k < nattn; ++k) {
+    const astraea_attn_phase* at = ats + k;
     const astraea_kv_geometry& g = at->geo;
-    if (!deep || !at->pool_dev || !at->q_dev || !at->table_dev || !at->ctx_dev || !at->out_dev ||
-        g.block_tokens != 16 || g.num_kv_heads <= 0 || g.num_kv_heads > 32 || at->num_q_heads % g.num_kv_heads ||
-        at->layer < 0 || at->layer >= g.num_layers || at->max_blocks <= 0)
+    if (!at->pool_dev || !at->q_dev || !at->table_dev || !at->ctx_dev || !at->out_dev || g.block_tokens != 16 ||
+        g.num_kv_heads <= 0 || g.num_kv_heads > 32 || at->num_q_heads % g.num_kv_heads || at->layer < 0 ||
+        at->layer >= g.num_layers || at->max_blocks <= 0 || attn_before[k] < 0 || attn_before[k] >= nph ||
+        (k && attn_before[k] <= attn_before[k - 1]))
       return ASTRAEA_EINVAL;
     const int G = at->num_q_heads / g.num_kv_heads, D = g.head_dim;
-    a.attn = (D == 128 && G == 4) ? 1 : (D == 64 && G == 2) ? 2 : (D == 64 && G == 4) ? 3 : 0;
-    if (!a.attn || num_sms() > 192) return ASTRAEA_EUNSUPPORTED;
-    attn::AttnWork& w = a.at;
+    a.attn_kind[k] = (D == 128 && G == 4) ? 1 : (D == 64 && G == 2) ? 2 : (D == 64 && G == 4) ? 3 : 0;
+    if (!a.attn_kind[k] || num_sms() > 192) return ASTRAEA_EUNSUPPORTED;
+    a.attn_before[k] = attn_before[k];
+    attn::AttnWork& w = a.at[k];
     w.pool = (const bf16*)at->pool_dev;
     w.block_el = (long long)astraea_kv_block_bytes(&g) / 2;
     w.layer = at->layer;
@@ -1261,21 +1274,22 @@ static int run_chain(int M, int nph, const astraea_gemm_phase* ph, void* ws, siz
     w.out = (bf16*)at->out_dev;
     w.scale_log2 = at->scale * 1.4426950408889634f;
     w.ws = (unsigned long long*)((char*)ws + kCounterBytes + kPhaseBytes);
-    w.tag = 0;   // set on the device from the launch epoch
+    w.tag = 0;        // set on the device from the launch epoch
     w.prefetch = 0;   // no wait before the page loads: nothing to overlap
     static const int min_pages = [] {
       const char* e = getenv("ASTRAEA_CHAIN_ATTN_MIN_PAGES");
       return e ? std::max(1, atoi(e)) : 2;   // pages per warp: measured best at batch 1-16
     }();
     w.min_pages = min_pages;
+    w.M = M;
+    if (ph[attn_before[k]].A != at->out_dev) return ASTRAEA_EINVAL;   // the attention output is that phase's A
     static const bool pf = [] {
       const char* e = getenv("ASTRAEA_CHAIN_KV_PREFETCH");
       return e && e[0] == '1';   // measured neutral at batch 1, -3% at batch 16: off
     }();
     a.pf_layer = (pf && at->layer + 1 < g.num_layers) ? at->layer + 1 : -1;
-    w.M = M;
-    if (ph[0].A != at->out_dev) return ASTRAEA_EINVAL;   // the attention output is phase 0's input
   }
+  a.nattn = nattn;
   a.M = M;
   a.grid = num_sms();
   a.nph = nph;
@@ -1327,10 +1341,11 @@ extern "C" int astraea_gemm_chain(int32_t M, int32_t nphases, const astraea_gemm
   return run_chain(M, nphases, phases, ws, ws_bytes, true, (cudaStream_t)stream);
 }
 
-extern "C" int astraea_gemm_chain_attn(int32_t M, const astraea_attn_phase* attn, int32_t nphases,
-                                       const astraea_gemm_phase* phases, void* ws, size_t ws_bytes, void* stream) {
-  if (!phases || !attn) return ASTRAEA_EINVAL;
-  return run_chain(M, nphases, phases, ws, ws_bytes, true, (cudaStream_t)stream, attn);
+extern "C" int astraea_gemm_chain_attn(int32_t M, int32_t nattn, const astraea_attn_phase* attn,
+                                       const int32_t* attn_before, int32_t nphases, const astraea_gemm_phase* phases,
+                                       void* ws, size_t ws_bytes, void* stream) {
+  if (!phases || !attn || nattn <= 0) return ASTRAEA_EINVAL;
+  return run_chain(M, nphases, phases, ws, ws_bytes, true, (cudaStream_t)stream, nattn, attn, attn_before);
 }
 
 extern "C" int astraea_gemm_bf16_ex(const void* A, int32_t lda, const void* W, int32_t ldw, void* C, int32_t ldc,

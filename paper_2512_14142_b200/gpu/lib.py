@@ -158,7 +158,8 @@ SIGNATURES = {
     "astraea_gemm_chain_workspace_bytes": (_sz, [_i32, _i32, ctypes.POINTER(GemmPhase)]),
     "astraea_gemm_chain": (ctypes.c_int, [_i32, _i32, ctypes.POINTER(GemmPhase), _vp, _sz, _vp]),
     "astraea_gemm_chain_attn": (
-        ctypes.c_int, [_i32, ctypes.POINTER(AttnPhase), _i32, ctypes.POINTER(GemmPhase), _vp, _sz, _vp]),
+        ctypes.c_int, [_i32, _i32, ctypes.POINTER(AttnPhase), ctypes.POINTER(_i32), _i32, ctypes.POINTER(GemmPhase),
+                       _vp, _sz, _vp]),
     "astraea_step_program_bytes": (_sz, [_i32]),
     "astraea_step_workspace_bytes": (_sz, [_i32, _i32, ctypes.POINTER(StepPhase)]),
     "astraea_step_program_build": (ctypes.c_int, [_i32, _i32, ctypes.POINTER(StepPhase), _vp, _sz, _vp, _sz]),

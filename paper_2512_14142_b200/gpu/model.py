@@ -216,6 +216,10 @@ class LlamaRunner:
         self.device = dev
         self.parts = -(-d // 128)
         self.use_chain = True   # decode GEMMs as one persistent chain per layer (False: one launch each)
+        # decoder layers per chain launch (with fused attention; 1 or 2). 2
+        # measured equal at batch 1-16 (the launch boundary costs what an
+        # in-kernel phase barrier costs under PDL), so 1 keeps the launches small
+        self.chain_layers = 1
         # decode step as ONE persistent kernel (astraea_step_launch). Off by
         # default: on B200 it matches the per-layer chain at batch 1 and trails
         # it at larger batches ("decode-step kernel")
@@ -310,11 +314,12 @@ class LlamaRunner:
         """One decode step for B rows (retired rows: slot -1, ctx 0). With
         ``keys_out`` the sampled tokens stay on the device as argmax keys.
 
-        Launches: embedding, RoPE table, layer 0's QKV GEMM, then per layer
-        ONE kernel running the paged attention and the chained GEMMs O-proj
-        -> gate/up -> down -> next layer's QKV (the last layer's chain ends
-        with lm_head + argmax instead); with fuse_attention off the
-        attention is a separate launch (2 per layer)."""
+        Launches: embedding, RoPE table, layer 0's QKV GEMM, then per
+        ``chain_layers`` (1) layer(s) ONE kernel running, for each layer, the
+        paged attention and the chained GEMMs O-proj -> gate/up -> down ->
+        next layer's QKV (the last layer ends with lm_head + argmax
+        instead); with fuse_attention off the attention is a separate
+        launch and each chain carries one layer."""
         if self.cfg.num_layers < 1 or tokens.shape[0] > 64:
             return self._decode_unchained(tokens, positions, slots, table, ctx, stream, want_logits, keys_out)
         if self.use_step_kernel and self._step_supported():
@@ -346,23 +351,29 @@ class LlamaRunner:
 
         ops.gemm_ex(**qkv(0, ssq0), workspace=ws, stream=stream)
         fuse = self.fuse_attention and self._attn_fusable()
-        for li, lw in enumerate(w.layers):
-            if not fuse:
-                ops.decode_attention(pool.geo, pool.data, li, q, qd, B, cfg.num_q_heads, table, ctx, self.scale,
-                                     att, dws, stream=stream)
-            phases = [
-                dict(a=att, w=lw["wo"], out=x, kind=L.EPI_RESIDUAL, residual=x, ssq_out=ssq_mid),
-                dict(a=x, w=lw["wgu"], out=h, kind=L.EPI_SILU, ssq_in=ssq_mid, rms_dim=d, rms_eps=eps),
-                dict(a=h, w=lw["wdown"], out=x, kind=L.EPI_RESIDUAL, residual=x, ssq_out=ssq),
-            ]
-            if li + 1 < cfg.num_layers:
-                phases.append(qkv(li + 1, ssq))
-            else:
-                phases.append(dict(a=x, w=w.lm_head, out=None, kind=L.EPI_ARGMAX, ssq_in=ssq, rms_dim=d, rms_eps=eps,
-                                   argmax_keys=keys))
-            attn = (dict(pool=pool.data, geo=pool.geo, layer=li, num_q_heads=cfg.num_q_heads, q=q, q_stride=qd,
-                         table=table, ctx=ctx, scale=self.scale, out=att) if fuse else None)
-            ops.gemm_chain(phases, ws, stream=stream, attn=attn)
+        per = self.chain_layers if fuse else 1
+        for l0 in range(0, cfg.num_layers, per):
+            phases, attns = [], []
+            for li in range(l0, min(l0 + per, cfg.num_layers)):
+                lw = w.layers[li]
+                if fuse:
+                    attns.append(dict(pool=pool.data, geo=pool.geo, layer=li, num_q_heads=cfg.num_q_heads, q=q,
+                                      q_stride=qd, table=table, ctx=ctx, scale=self.scale, out=att,
+                                      before=len(phases)))
+                else:
+                    ops.decode_attention(pool.geo, pool.data, li, q, qd, B, cfg.num_q_heads, table, ctx,
+                                         self.scale, att, dws, stream=stream)
+                phases += [
+                    dict(a=att, w=lw["wo"], out=x, kind=L.EPI_RESIDUAL, residual=x, ssq_out=ssq_mid),
+                    dict(a=x, w=lw["wgu"], out=h, kind=L.EPI_SILU, ssq_in=ssq_mid, rms_dim=d, rms_eps=eps),
+                    dict(a=h, w=lw["wdown"], out=x, kind=L.EPI_RESIDUAL, residual=x, ssq_out=ssq),
+                ]
+                if li + 1 < cfg.num_layers:
+                    phases.append(qkv(li + 1, ssq))
+                else:
+                    phases.append(dict(a=x, w=w.lm_head, out=None, kind=L.EPI_ARGMAX, ssq_in=ssq, rms_dim=d,
+                                       rms_eps=eps, argmax_keys=keys))
+            ops.gemm_chain(phases, ws, stream=stream, attn=attns or None)
         if keys_out is not None:
             return keys_out
         return ops.keys_to_ids(keys)

@@ -87,8 +87,10 @@ def gemm_chain(phases, workspace, stream=None, attn=None):
     ``phases``: list of dicts with a, w, out and the ``gemm_ex`` epilogue
     keywords; every ``a`` has the same number of rows (M <= 64). ``attn``
     (optional dict: pool, geo, layer, num_q_heads, q, q_stride, table, ctx,
-    scale, out): the layer's decode attention runs first in the same launch
-    (astraea_gemm_chain_attn); its ``out`` must be phase 0's ``a``."""
+    scale, out, and ``before``, default 0; or a list of up to two such
+    dicts): a layer's decode attention runs right before GEMM phase
+    ``before`` in the same launch (astraea_gemm_chain_attn); its ``out``
+    must be that phase's ``a``."""
     lib = L.require_cuda()
     n = len(phases)
     arr = (L.GemmPhase * n)()
@@ -108,12 +110,17 @@ def gemm_chain(phases, workspace, stream=None, attn=None):
         L.check(lib.astraea_gemm_chain(M, n, arr, L.ptr(workspace), workspace.numel() * workspace.element_size(),
                                        _s(stream)), "gemm_chain")
     else:
-        at = L.AttnPhase()
-        at.pool_dev, at.geo, at.layer = L.ptr(attn["pool"]), attn["geo"], attn["layer"]
-        at.num_q_heads, at.q_dev, at.q_row_stride = attn["num_q_heads"], L.ptr(attn["q"]), attn["q_stride"]
-        at.table_dev, at.max_blocks = L.ptr(attn["table"]), attn["table"].shape[1]
-        at.ctx_dev, at.scale, at.out_dev = L.ptr(attn["ctx"]), attn["scale"], L.ptr(attn["out"])
-        L.check(lib.astraea_gemm_chain_attn(M, ctypes.byref(at), n, arr, L.ptr(workspace),
+        attns = attn if isinstance(attn, (list, tuple)) else [attn]
+        ats = (L.AttnPhase * len(attns))()
+        before = (ctypes.c_int32 * len(attns))()
+        for k, d in enumerate(attns):
+            at = ats[k]
+            at.pool_dev, at.geo, at.layer = L.ptr(d["pool"]), d["geo"], d["layer"]
+            at.num_q_heads, at.q_dev, at.q_row_stride = d["num_q_heads"], L.ptr(d["q"]), d["q_stride"]
+            at.table_dev, at.max_blocks = L.ptr(d["table"]), d["table"].shape[1]
+            at.ctx_dev, at.scale, at.out_dev = L.ptr(d["ctx"]), d["scale"], L.ptr(d["out"])
+            before[k] = d.get("before", 0)
+        L.check(lib.astraea_gemm_chain_attn(M, len(attns), ats, before, n, arr, L.ptr(workspace),
                                             workspace.numel() * workspace.element_size(), _s(stream)),
                 "gemm_chain_attn")
     _count()

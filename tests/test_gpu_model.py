@@ -122,10 +122,12 @@ def test_kv_action_invariance_preserve_swap_discard():
     assert p[2][:49] == d[2][:49]                              # segment-1 context re-fed exactly
 
 
+@pytest.mark.parametrize("chain_layers", [1, 2])
 @pytest.mark.parametrize("B", [1, 4])
-def test_chained_decode_step_equals_unchained(B):
-    """The 2-launches-per-layer decode step is bit-identical to the
-    one-launch-per-GEMM step (same tokens, same KV written)."""
+def test_chained_decode_step_equals_unchained(B, chain_layers):
+    """The chained decode step (attention fused, 1 or 2 layers per launch)
+    is bit-identical to the one-launch-per-GEMM step (same tokens, same KV
+    written)."""
     cfg = PRESETS["small"]
     w = LlamaWeights(cfg, seed=4)
     d = lambda v: torch.tensor(v, dtype=torch.int32, device=DEV)  # noqa: E731
@@ -134,6 +136,7 @@ def test_chained_decode_step_equals_unchained(B):
         pool = KvPool(cfg, 64)
         runner = LlamaRunner(w, pool)
         runner.use_step_kernel = False
+        runner.chain_layers = chain_layers
         for b in range(B):
             ids = segment_token_ids(f"c{b}", 1, 20 + b, cfg.vocab)
             _prefill_one(runner, pool, ids, [4 * b, 4 * b + 1, 4 * b + 2, 4 * b + 3])

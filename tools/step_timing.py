@@ -1,5 +1,6 @@
-"""Decode-step time of Llama-3-8B at a given batch/context: the one-launch
-step kernel (several L2 look-ahead depths) vs the per-layer launch path.
+"""Decode-step time of Llama-3-8B at a given batch/context: chained launches
+carrying 1 or 2 layers each, optionally the one-launch step kernel (several
+L2 look-ahead depths).
 Prints one JSON line per variant with ms/step and HBM GB/s (weights + KV)."""
 import argparse
 import json
@@ -17,7 +18,8 @@ ap.add_argument("--model", default="llama3-8b")
 ap.add_argument("--batch", type=int, nargs="+", default=[1, 4, 16])
 ap.add_argument("--ctx", type=int, default=900)
 ap.add_argument("--steps", type=int, default=20)
-ap.add_argument("--l2", type=int, nargs="+", default=[0, 8, 24])
+ap.add_argument("--l2", type=int, nargs="*", default=[])
+ap.add_argument("--chain-layers", type=int, nargs="+", default=[1, 2])
 a = ap.parse_args()
 cfg = PRESETS[a.model]
 w = LlamaWeights(cfg)
@@ -33,10 +35,12 @@ for B in a.batch:
     slots = table[:, a.ctx // 16] * 16 + a.ctx % 16
     ctxd = torch.full((B,), a.ctx + 1, dtype=torch.int32, device="cuda")
     keys = torch.zeros(B, dtype=torch.int64, device="cuda")
-    variants = [("layers", False, 0)] + [(f"step_l2_{l}", True, l) for l in a.l2]
-    for name, step_kernel, l2 in variants:
+    variants = ([(f"chain_{c}", False, 0, c) for c in a.chain_layers] +
+                [(f"step_l2_{l}", True, l, 1) for l in a.l2])
+    for name, step_kernel, l2, cl in variants:
         r.use_step_kernel = step_kernel
         r.l2_ahead = l2
+        r.chain_layers = cl
         for _ in range(3):
             r.decode(tok, pos, slots, table, ctxd, keys_out=keys)
         torch.cuda.synchronize()
