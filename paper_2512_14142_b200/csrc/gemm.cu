@@ -354,7 +354,9 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_cluster) {
 
 // Partial sums of the other K-splits of a tile, added to each 32-column chunk
 // the finisher (split 0) loads from TMEM: self-validating 64-bit words
-// (fp32 bits | tag << 32), one spin per word.
+// (fp32 bits | tag << 32), stale words re-polled together. Partials are column-major
+// ([256 cols][128 rows] per CTA and split): a warp's lanes are consecutive
+// rows, so every load and store is coalesced.
 struct PairSplitFix {
   const unsigned long long* base;   // (tile, split 1, this CTA) row `row`
   long long stride;                 // between splits
@@ -362,15 +364,21 @@ struct PairSplitFix {
   unsigned tag;
   __device__ __forceinline__ void operator()(float* v, int col) const {
     for (int s = 0; s < extra; ++s) {
-      const unsigned long long* p = base + s * stride + col;
+      const unsigned long long* p = base + s * stride + (long long)col * 128;
       unsigned long long w[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) w[j] = ld_relaxed_u64(p + j);
+      for (int j = 0; j < 32; ++j) w[j] = ld_relaxed_u64(p + j * 128);
+      for (;;) {   // stale words re-polled together
+        bool ready = true;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        while ((unsigned)(w[j] >> 32) != tag) w[j] = ld_relaxed_u64(p + j);
-        v[j] += __uint_as_float((unsigned)w[j]);
+        for (int j = 0; j < 32; ++j) ready &= (unsigned)(w[j] >> 32) == tag;
+        if (ready) break;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if ((unsigned)(w[j] >> 32) != tag) w[j] = ld_relaxed_u64(p + j * 128);
       }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] += __uint_as_float((unsigned)w[j]);
     }
   }
 };
@@ -495,19 +503,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (sp > 0) {
         // contributor: publish this split's accumulator rows as tagged partials
         unsigned long long* p =
-            args.part + (((long long)t * (S - 1) + (sp - 1)) * 2 + rank) * kPartCta + (long long)row_local * 256;
+            args.part + (((long long)t * (S - 1) + (sp - 1)) * 2 + rank) * kPartCta + row_local;
         for (int c = 0; c < 8; ++c) {
           float v[32];
           tmem_ld32(taddr + c * 32, v);
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            st_relaxed_u64(p + c * 32 + j,
+            st_relaxed_u64(p + (c * 32 + j) * 128,
                            (unsigned long long)__float_as_uint(v[j]) | ((unsigned long long)tag << 32));
         }
       } else {
         const float rs = (e.ssq_in && mok) ? rms_scale(e, args.M, m) : 1.f;
         if (S > 1) {
-          PairSplitFix fix{args.part + ((long long)t * (S - 1) * 2 + rank) * kPartCta + (long long)row_local * 256,
+          PairSplitFix fix{args.part + ((long long)t * (S - 1) * 2 + rank) * kPartCta + row_local,
                            2 * kPartCta, S - 1, tag};
           rows_epilogue<256>(args, m, mok, rs, taddr, tn, fix);
         } else {
@@ -611,6 +619,49 @@ struct ChainArgs {
 constexpr int kAttnCtr = kMaxPhases + 2;   // phase_ctr slots kAttnCtr + k: CTAs done with attention k
 
 
+// Stream-K fix-up loads of a split tile's finisher: the words of segments
+// c_first+1..c_last for tokens T0 <= t < min(M, T0 + MT) (compile-time
+// range), 32/MT segments per round. All words of a round are loaded together and the stale
+// ones (tag not yet this launch's) re-polled together: a late segment costs
+// one round trip after it lands, not one per word. Summed in CTA order.
+template <int MT, int T0, int BN>
+__device__ __forceinline__ void sk_collect(const unsigned long long* tpart, int c_first, int c_last,
+                                           long long cstride, int M, unsigned tag, float (&acc)[BN]) {
+  static_assert(MT <= 32 && T0 + MT <= BN, "token range");
+  constexpr int KG = 32 / MT;
+  const unsigned long long ready_word = (unsigned long long)tag << 32;
+  for (int c0 = c_first + 1; c0 <= c_last; c0 += KG) {
+    unsigned long long pv[KG][MT];
+    const unsigned long long* base = tpart + (long long)(c0 - c_first) * cstride;
+#pragma unroll
+    for (int k = 0; k < KG; ++k)
+#pragma unroll
+      for (int t = 0; t < MT; ++t)
+        pv[k][t] = (c0 + k <= c_last && T0 + t < M) ? ld_relaxed_u64(base + k * cstride + (long long)(T0 + t) * kBM)
+                                                    : ready_word;
+    for (;;) {
+      bool ready = true;
+#pragma unroll
+      for (int k = 0; k < KG; ++k)
+#pragma unroll
+        for (int t = 0; t < MT; ++t) ready &= (unsigned)(pv[k][t] >> 32) == tag;
+      if (ready) break;
+#pragma unroll
+      for (int k = 0; k < KG; ++k)
+#pragma unroll
+        for (int t = 0; t < MT; ++t)
+          if ((unsigned)(pv[k][t] >> 32) != tag) pv[k][t] = ld_relaxed_u64(base + k * cstride + (long long)(T0 + t) * kBM);
+    }
+#pragma unroll
+    for (int k = 0; k < KG; ++k) {
+      if (c0 + k > c_last) break;
+#pragma unroll
+      for (int t = 0; t < MT; ++t)
+        if (T0 + t < M) acc[T0 + t] += __uint_as_float((unsigned)pv[k][t]);
+    }
+  }
+}
+
 __device__ __forceinline__ int sk_owner(long long u, long long units, int grid) {
   return (int)(((u + 1) * grid - 1) / units);
 }
@@ -638,8 +689,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
   bf16* xch = reinterpret_cast<bf16*>(tmem_slot + 4);        // [BN][128]
   float* red = reinterpret_cast<float*>(xch + BN * kBM);     // [4][BN]
   float* rs = red + 4 * BN;                                  // [BN]
+  int* slot_s = reinterpret_cast<int*>(rs + BN);             // [64] QKV phases: the tokens' pool slots
   constexpr bool kAttn = MINB == 1;                          // deep (layer) chains carry the attention phase
-  bf16* vs_all = reinterpret_cast<bf16*>((reinterpret_cast<uintptr_t>(rs + BN) + 127) & ~uintptr_t(127));
+  bf16* vs_all = reinterpret_cast<bf16*>((reinterpret_cast<uintptr_t>(slot_s + 64) + 127) & ~uintptr_t(127));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
@@ -817,10 +869,25 @@ __global__ void __launch_bounds__(kThreads, MINB)
           }
         }
       }
-      if (P.epi.ssq_in) {
-        if (row < args.M) rs[row] = rms_scale(P.epi, args.M, row);
-        epi_bar();
+      // per-phase token data staged in shared memory: RMS scales, and for a
+      // QKV phase the pool slots and (deep chains: in the attention's V-page
+      // space, free during the GEMM phases) the RoPE table -- the finisher's
+      // epilogue then reads no global memory but its outputs' inputs
+      const bool qkv = P.epi.kind == EPI_QKV_ROPE;
+      const float2* cs_s = nullptr;
+      bool stage = false;
+      if constexpr (kAttn) {
+        const int n = args.M * (P.epi.D / 2);
+        stage = qkv && P.epi.cs && n * (int)sizeof(float2) <= 4 * attn::kAttnWarpBytes;
+        if (stage) {
+          if (row < args.M) slot_s[row] = P.epi.slots[row];
+          float2* cs = reinterpret_cast<float2*>(vs_all);
+          for (int i = row; i < n; i += kBM) cs[i] = P.epi.cs[i];
+          cs_s = cs;
+        }
       }
+      if (P.epi.ssq_in && row < args.M) rs[row] = rms_scale(P.epi, args.M, row);
+      if (P.epi.ssq_in || stage) epi_bar();
       if constexpr (kAttn) {
         if (args.nattn && args.pf_layer >= 0 && p == args.nph - 1) {
           // the next layer's attention (next launch) reads these pages: warm L2 now
@@ -863,27 +930,22 @@ __global__ void __launch_bounds__(kThreads, MINB)
           }
 #pragma unroll
           for (int t = 0; t < BN; ++t) acc[t] = 0.f;
-          constexpr int GRP = 1;   // one segment's words in flight at a time (register budget; measured best)
-          for (int c0 = c_first + 1; c0 <= c_last; c0 += GRP) {
-            unsigned long long pv[GRP][BN];
-#pragma unroll
-            for (int k = 0; k < GRP; ++k) {
-              const unsigned long long* pp = tpart + (long long)(c0 + k - c_first) * args.M * kBM;
-#pragma unroll
-              for (int t = 0; t < BN; ++t)
-                pv[k][t] = (c0 + k <= c_last && t < args.M) ? ld_relaxed_u64(pp + (long long)t * kBM) : 0ull;
-            }
-#pragma unroll
-            for (int k = 0; k < GRP; ++k) {
-              if (c0 + k <= c_last) {
-                const unsigned long long* pp = tpart + (long long)(c0 + k - c_first) * args.M * kBM;
-#pragma unroll
-                for (int t = 0; t < BN; ++t) {
-                  if (t < args.M) {
-                    while ((unsigned)(pv[k][t] >> 32) != tag) pv[k][t] = ld_relaxed_u64(pp + (long long)t * kBM);
-                    acc[t] += __uint_as_float((unsigned)pv[k][t]);
-                  }
-                }
+          // the other segments' words: up to 32 per thread in flight (several
+          // segments at once when M is small), stale words re-polled together
+          const long long cstride = (long long)args.M * kBM;
+          const int M = args.M;
+          if (M <= 1) sk_collect<1, 0>(tpart, c_first, c_last, cstride, M, tag, acc);
+          else if (M <= 2) sk_collect<2, 0>(tpart, c_first, c_last, cstride, M, tag, acc);
+          else if (M <= 4) sk_collect<4, 0>(tpart, c_first, c_last, cstride, M, tag, acc);
+          else if (M <= 8) sk_collect<8, 0>(tpart, c_first, c_last, cstride, M, tag, acc);
+          else if (M <= 16) sk_collect<16, 0>(tpart, c_first, c_last, cstride, M, tag, acc);
+          else if constexpr (BN >= 32) {
+            sk_collect<16, 0>(tpart, c_first, c_last, cstride, M, tag, acc);
+            sk_collect<16, 16>(tpart, c_first, c_last, cstride, M, tag, acc);
+            if constexpr (BN == 64) {
+              if (M > 32) {
+                sk_collect<16, 32>(tpart, c_first, c_last, cstride, M, tag, acc);
+                sk_collect<16, 48>(tpart, c_first, c_last, cstride, M, tag, acc);
               }
             }
           }
@@ -909,7 +971,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
 #pragma unroll
           for (int t = 0; t < BN; ++t) v[t] = acc[t] + v[t];
         }
-        sk_finish<BN>(P, (int)tile, row, v, rs, xch, red, (kPreRes && resid) ? res : nullptr);
+        sk_finish<BN>(P, (int)tile, row, v, rs, xch, red, (kPreRes && resid) ? res : nullptr, stage ? slot_s : nullptr,
+                      cs_s);
       }
       // phase p done in this CTA: publish (release) for the other CTAs
       epi_bar();
@@ -1031,7 +1094,8 @@ size_t partial_bytes(int M, const SkPlan& p) { return (size_t)p.tiles * p.maxseg
 template <int BN, bool DEEP = false>
 constexpr size_t sk_extra_bytes() {
   // DEEP (layer) chains also hold the attention phase's four V pages
-  return (size_t)BN * kBM * 2 + 5 * BN * sizeof(float) + 64 + (DEEP ? 128 + 4 * (size_t)attn::kAttnWarpBytes : 0);
+  return (size_t)BN * kBM * 2 + 5 * BN * sizeof(float) + 64 * sizeof(int) + 64 +
+         (DEEP ? 128 + 4 * (size_t)attn::kAttnWarpBytes : 0);
 }
 // Single GEMMs: ~104 KB so two CTAs fit per SM and the next kernel's CTA can
 // become resident and prefetch its weights (PDL) while this one drains.

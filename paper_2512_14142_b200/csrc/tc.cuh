@@ -152,12 +152,14 @@ __device__ __forceinline__ float rms_scale(const Epi& e, int M, int t) {
 }
 
 // Destination of a rotated/plain head element in QKV_ROPE: q -> C, k/v -> pool.
-__device__ __forceinline__ void qkv_store(const Epi& e, bf16* C, int ldc, int t, int head, int hrow, float y) {
+// slot_pre: token t's pool slot when the caller staged it (>= -1), else -2
+__device__ __forceinline__ void qkv_store(const Epi& e, bf16* C, int ldc, int t, int head, int hrow, float y,
+                                          int slot_pre = -2) {
   if (head < e.Hq) {
     C[(long long)t * ldc + head * e.D + hrow] = f2bf(y);
     return;
   }
-  const int slot = e.slots[t];
+  const int slot = slot_pre >= -1 ? slot_pre : e.slots[t];
   if (slot < 0) return;
   const int kv = head < e.Hq + e.Hkv ? 0 : 1;
   const int h = head - e.Hq - kv * e.Hkv;
@@ -201,7 +203,10 @@ __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned l
 // tile*128 + row. All 128 epilogue threads call this together.
 template <int BN, typename A>
 __device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* v, const float* rs,
-                                          bf16* xch, float* red, const float* res_pre = nullptr) {
+                                          bf16* xch, float* red, const float* res_pre = nullptr,
+                                          const int* slot_s = nullptr, const float2* cs_s = nullptr) {
+  // slot_s / cs_s (optional): the tokens' pool slots and the [M][D/2] RoPE
+  // table staged in shared memory by the caller (QKV_ROPE)
   const Epi& e = a.epi;
   const int M = a.M;
   const int f = tile * kBM + row;
@@ -274,10 +279,10 @@ __device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* 
         float y = x;
         if (rot) {
           const float xp = bf2f(xch[t * kBM + partner]);
-          const float2 r = rope_cs(e, t, hrow % half);
+          const float2 r = cs_s ? cs_s[t * half + hrow % half] : rope_cs(e, t, hrow % half);
           y = hrow < half ? x * r.x - xp * r.y : x * r.x + xp * r.y;
         }
-        qkv_store(e, a.C, a.ldc, t, head, hrow, y);
+        qkv_store(e, a.C, a.ldc, t, head, hrow, y, slot_s ? slot_s[t] : -2);
       }
     }
   }

@@ -19,6 +19,7 @@ ap.add_argument("--batch", type=int, default=1)
 ap.add_argument("--ctx", type=int, default=900)
 ap.add_argument("--layers", type=int, nargs="+", default=[0, 1, 2, 16, 31])
 ap.add_argument("--no-fuse", action="store_true")
+ap.add_argument("--per-cta", action="store_true")
 a = ap.parse_args()
 cfg = PRESETS["llama3-8b"]
 w = LlamaWeights(cfg)
@@ -73,3 +74,14 @@ for i in range(n):
         sp = s[:, 16 + 14]
         att["m_group0_spins_max"] = int(sp.max())
         print(json.dumps({"layer": li, "attention_warp0_first_piece": att}))
+
+if a.per_cta:
+    # per-CTA phase completion (relative to the phase's activation release) of one launch
+    i = a.layers[-1] + 1
+    s = t[i]
+    for p, nm in enumerate(names):
+        rel = float(s[:, 1 + p][s[:, 1 + p] > 0].median())
+        done = (s[:, 5 + p] - rel) / 1000
+        order = torch.argsort(done, descending=True)[:12]
+        print(json.dumps({"phase": nm, "median_us": round(float(done.median()), 2),
+                          "slowest": [[int(c), round(float(done[c]), 2)] for c in order]}))
