@@ -435,7 +435,7 @@ def decode_step_gbs(dp, cfg, B, ctx):
     e1.record()
     e1.synchronize()
     ms = e0.elapsed_time(e1) / n
-    by = cfg.weight_bytes + B * (ctx + 1) * cfg.kv_bytes_per_token
+    by = cfg.decode_weight_bytes + B * (ctx + 1) * cfg.kv_bytes_per_token
     return by / (ms / 1000.0) / 1e9, ms
 
 

@@ -467,28 +467,33 @@ __device__ __forceinline__ void attn_cta_phase(const AttnWork& A, int cta, int g
             for (int e = 0; e < EPT; ++e) ready &= (unsigned)(po[k][e] >> 32) == A.tag;
           }
           if (ready) {
-            if (atr && lane == 0 && first_piece && c0 == first_c + 1) {
-              atr[13] = gtimer_();
-              atr[14] = (unsigned long long)spin;
-            }
+            if (atr && lane == 0 && first_piece && c0 == first_c + 1) atr[14] = (unsigned long long)spin;
             break;
           }
           __nanosleep(64);
         }
+        if (atr && first_piece && c0 == first_c + 1) {
+          __syncwarp();
+          if (lane == 0) atr[13] = gtimer_();   // every lane of the warp has its words
+        }
+        // a thread's EPT elements share one head row: one (m, l) rescale per part
+        float mc = Mv[0], lc = Lv[0];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          if (c0 + k > last_c) break;
+          if (c0 + k > last_c) continue;   // warp-uniform
           const float mk = __uint_as_float((unsigned)pm[k]), lk = __uint_as_float((unsigned)pl[k]);
+          const float mn = fmaxf(mc, mk);
+          const float mr = mn == -INFINITY ? 0.f : mn;   // all -inf: both scales 0
+          const float a0 = exp2f(mc - mr), a1 = exp2f(mk - mr);
+          lc = lc * a0 + lk * a1;
 #pragma unroll
-          for (int e = 0; e < EPT; ++e) {
-            if (et * EPT + e >= G * D) continue;
-            const float mn = fmaxf(Mv[e], mk);
-            const float a0 = mn == -INFINITY ? 0.f : exp2f(Mv[e] - mn);
-            const float a1 = mn == -INFINITY ? 0.f : exp2f(mk - mn);
-            Lv[e] = Lv[e] * a0 + lk * a1;
-            Ov[e] = Ov[e] * a0 + __uint_as_float((unsigned)po[k][e]) * a1;
-            Mv[e] = mn;
-          }
+          for (int e = 0; e < EPT; ++e) Ov[e] = Ov[e] * a0 + __uint_as_float((unsigned)po[k][e]) * a1;
+          mc = mn;
+        }
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+          Mv[e] = mc;
+          Lv[e] = lc;
         }
       }
       done = true;

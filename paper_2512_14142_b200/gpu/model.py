@@ -55,6 +55,16 @@ class LlamaConfig:
         return 2 * (L * per_layer + 2 * self.vocab * d + d)
 
     @property
+    def decode_weight_bytes(self) -> int:
+        """Weight bytes one decode step must read: every layer, the final norm
+        and lm_head; of the embedding table only the B gathered rows (not
+        counted here)."""
+        d, L = self.hidden, self.num_layers
+        per_layer = (self.qkv_dim * d + d * self.num_q_heads * self.head_dim
+                     + 2 * self.ffn * d + d * self.ffn + 2 * d)
+        return 2 * (L * per_layer + self.vocab * d + d)
+
+    @property
     def linear_params_per_token(self) -> int:
         """Multiply-adds per token in the layer projections (prefill FLOPs / 2)."""
         d = self.hidden

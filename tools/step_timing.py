@@ -51,6 +51,6 @@ for B in a.batch:
         e1.record()
         e1.synchronize()
         ms = e0.elapsed_time(e1) / a.steps
-        by = cfg.weight_bytes + B * (a.ctx + 1) * cfg.kv_bytes_per_token
+        by = cfg.decode_weight_bytes + B * (a.ctx + 1) * cfg.kv_bytes_per_token
         print(json.dumps({"B": B, "ctx": a.ctx, "variant": name, "ms": round(ms, 4),
                           "hbm_gbs": round(by / ms / 1e6, 1)}), flush=True)
