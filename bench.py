@@ -13,7 +13,8 @@ swap-out/in the KV policy orders, executed on the GPU.
   e2e        requests/s through the public API (GpuEngine.run) timed on the
              host clock, prompt ids uploaded from pinned host memory per batch
              and generated tokens read back per batch (bytes reported);
-  roofline   the dominant kernel (decode-mode tcgen05 GEMM, weight stream)
+  roofline   the dominant kernel (one decoder layer's fused launch: paged
+             attention + the chained tcgen05 GEMMs, weight + KV stream)
              against measured HBM bandwidth;
   cpu_baseline  the CPU port (oracle/cpu_baseline.py) on a bounded sample.
 
@@ -310,13 +311,14 @@ def main():
     mrep = GpuEngine(shard, pol, pred, mem, scfg, dp, clock="measured").run()
     agg = mrep.aggregates()
 
-    # ---- dominant kernel: the chained decode GEMM (one layer's O -> gate/up ->
-    # down -> next QKV in one persistent tcgen05 launch) at the replay's mean
-    # batch, timed with CUDA events on its stream; algorithmic bytes = the four
-    # weight matrices + activations in/out per launch
+    # ---- dominant kernel: one decoder layer's fused launch (paged attention ->
+    # O -> gate/up -> down -> next QKV in one persistent tcgen05 kernel) at the
+    # replay's mean batch and context, timed with CUDA events on its stream;
+    # algorithmic bytes = the four weight matrices + the layer's K/V pages +
+    # activations in/out per launch
     hbm, peak_kind = peaks()
     B = max(1, int(round(work["mean_batch"])))
-    chain_ms, chain_bytes = chain_kernel_time(dp, cfg, B)
+    chain_ms, chain_bytes, chain_ctx = chain_kernel_time(dp, cfg, B, int(work["mean_ctx"]))
     gemm_gbs = chain_bytes / (chain_ms / 1000.0) / 1e9
     traffic = profiled_traffic(B)
 
@@ -339,7 +341,8 @@ def main():
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": gemm_gbs, "peak": hbm, "unit": "GB/s", "frac": gemm_gbs / hbm,
                      "traffic": traffic,
-                     "kernel": f"gemm_chain_kernel (layer O->GU->Down->QKV, tcgen05 stream-K), M={B}",
+                     "kernel": f"gemm_chain_kernel (layer: paged attention -> O -> GU -> Down -> next QKV, "
+                               f"tcgen05 stream-K), M={B}, ctx={chain_ctx}",
                      "algorithmic_bytes_per_launch": chain_bytes, "launch_ms": chain_ms,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, copy burst)"},
         "jct_measured_clock": {"avg_s": agg["avg_jct"], "p99_s": agg["p99_jct"],
@@ -359,25 +362,34 @@ def main():
     barrier(world)
 
 
-def chain_kernel_time(dp, cfg, B, reps=50):
-    """One layer's chained decode GEMMs exactly as LlamaRunner.decode issues
-    them (O + residual, gate/up + SiLU, down + residual, next layer's QKV +
-    RoPE + KV append)."""
+def chain_kernel_time(dp, cfg, B, ctx, reps=50):
+    """One decoder layer's fused launch exactly as LlamaRunner.decode issues
+    it: the paged decode attention (B rows x ctx tokens) followed by the
+    chained O + residual, gate/up + SiLU, down + residual and next layer's
+    QKV + RoPE + KV append, one persistent tcgen05 kernel. Returns (ms per
+    launch, algorithmic bytes per launch = the four weight matrices + the
+    layer's K/V pages + activations in/out, context actually used)."""
     import torch
     from paper_2512_14142_b200.gpu import lib as L
     from paper_2512_14142_b200.gpu import ops
-    w, pool = dp.weights, dp.pool
+    w, pool, r = dp.weights, dp.pool, dp.runner
     d, F, qd = cfg.hidden, cfg.ffn, cfg.num_q_heads * cfg.head_dim
     lw, lw1 = w.layers[0], w.layers[1 % cfg.num_layers]
     dev = "cuda"
+    nb = (ctx + 16) // 16
+    if B * nb > pool.num_blocks:   # the bench's pool is sized for its capacity: shorten the context
+        nb = max(1, pool.num_blocks // B)
+        ctx = nb * 16 - 1
     x = torch.randn(B, d, device=dev).bfloat16()
-    att = torch.randn(B, qd, device=dev).bfloat16()
+    q = (torch.randn(B, qd, device=dev) * 0.5).bfloat16()
+    att = torch.empty(B, qd, device=dev).bfloat16()
     h = torch.empty(B, F, device=dev).bfloat16()
-    q = torch.empty(B, qd, device=dev).bfloat16()
     s1 = torch.empty(-(-d // 128), B, device=dev)
     s2 = torch.empty(-(-d // 128), B, device=dev)
-    pos = torch.full((B,), 100, dtype=torch.int32, device=dev)
-    slots = torch.full((B,), -1, dtype=torch.int32, device=dev)   # no KV written
+    pos = torch.full((B,), ctx, dtype=torch.int32, device=dev)
+    slots = torch.full((B,), -1, dtype=torch.int32, device=dev)   # no KV written: every launch reads the same
+    table = torch.arange(B * nb, dtype=torch.int32, device=dev).view(B, nb)
+    ctxd = torch.full((B,), ctx + 1, dtype=torch.int32, device=dev)
     cs = ops.rope_table(pos, cfg.head_dim, cfg.rope_theta)
     phases = [dict(a=att, w=lw["wo"], out=x, kind=L.EPI_RESIDUAL, residual=x, ssq_out=s1),
               dict(a=x, w=lw["wgu"], out=h, kind=L.EPI_SILU, ssq_in=s1, rms_dim=d, rms_eps=cfg.eps),
@@ -385,21 +397,24 @@ def chain_kernel_time(dp, cfg, B, reps=50):
               dict(a=x, w=lw1["wqkv"], out=q, kind=L.EPI_QKV_ROPE, ssq_in=s2, rms_dim=d, rms_eps=cfg.eps,
                    pool=pool.data, geo=pool.geo, layer=1 % cfg.num_layers, num_q_heads=cfg.num_q_heads,
                    positions=pos, slots=slots, rope_theta=cfg.rope_theta, rope_table=cs)]
-    ws = dp.runner.gemm_ws
+    attn = (dict(pool=pool.data, geo=pool.geo, layer=0, num_q_heads=cfg.num_q_heads, q=q, q_stride=qd,
+                 table=table, ctx=ctxd, scale=r.scale, out=att) if r.fuse_attention and r._attn_fusable() else None)
+    ws = r.gemm_ws
     s = torch.cuda.current_stream()
     for _ in range(3):
-        ops.gemm_chain(phases, ws, stream=s)
+        ops.gemm_chain(phases, ws, stream=s, attn=attn)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
     for _ in range(reps):
-        ops.gemm_chain(phases, ws, stream=s)
+        ops.gemm_chain(phases, ws, stream=s, attn=attn)
     e1.record(s)
     e1.synchronize()
     ms = e0.elapsed_time(e1) / reps
     wbytes = sum(ph["w"].numel() * 2 for ph in phases)
     act = 2 * B * (qd + d + d + F + F + d + d + qd)   # A in + C out per phase
-    return ms, wbytes + act
+    kv = B * (ctx + 1) * cfg.kv_bytes_per_token // cfg.num_layers if attn else 0
+    return ms, wbytes + act + kv, ctx
 
 
 def profiled_traffic(B):
