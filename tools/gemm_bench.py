@@ -1,5 +1,5 @@
 """Prefill-GEMM throughput (tcgen05) at Llama-3-8B projection shapes:
-TFLOP/s per (M, N, K) with CUDA events. ASTRAEA_GEMM_PAIR=0 selects the
+TFLOP/s per (M, N, K) with CUDA events around a CUDA graph of 20 launches. ASTRAEA_GEMM_PAIR=0 selects the
 one-CTA kernel instead of the CTA-pair kernel."""
 import json
 import os
@@ -25,9 +25,16 @@ for M in Ms:
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         n = 20
+        # n back-to-back launches in one CUDA graph: device time, not the
+        # host's per-call launch overhead (which alone is ~25 us per call)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(n):
+                ops.gemm(a, w, out, workspace=ws)
+        g.replay()
+        torch.cuda.synchronize()
         e0.record()
-        for _ in range(n):
-            ops.gemm(a, w, out, workspace=ws)
+        g.replay()
         e1.record()
         e1.synchronize()
         us = e0.elapsed_time(e1) / n * 1000
