@@ -671,7 +671,7 @@ __device__ __forceinline__ void wait_phase(const int* ctr, int target) {
 }
 
 
-template <int BN, int STAGES, int MINB>
+template <int BN, int STAGES, int MINB, int MT = BN>   // MT: token loops' bound (1: batch of one)
 __global__ void __launch_bounds__(kThreads, MINB)
     gemm_chain_kernel(const __grid_constant__ ChainMaps maps, const __grid_constant__ ChainArgs args) {
   constexpr int A_BYTES = kBM * kBK * 2;
@@ -925,16 +925,19 @@ __global__ void __launch_bounds__(kThreads, MINB)
           if (kPreRes && resid) {
             const int f = (int)tile * kBM + row;
 #pragma unroll
-            for (int t = 0; t < BN; ++t)
+            for (int t = 0; t < MT; ++t)
               res[t] = (t < args.M && f < P.N) ? bf2f(__ldcg(P.epi.residual + (long long)t * P.ldc + f)) : 0.f;
           }
 #pragma unroll
-          for (int t = 0; t < BN; ++t) acc[t] = 0.f;
+          for (int t = 0; t < MT; ++t) acc[t] = 0.f;
           // the other segments' words: up to 32 per thread in flight (several
           // segments at once when M is small), stale words re-polled together
           const long long cstride = (long long)args.M * kBM;
           const int M = args.M;
-          if (M <= 1) sk_collect<1, 0>(tpart, c_first, c_last, cstride, M, tag, acc);
+          if (MT == 1 || M <= 1) sk_collect<1, 0>(tpart, c_first, c_last, cstride, M, tag, acc);
+          else if (MT == 2) sk_collect<2, 0>(tpart, c_first, c_last, cstride, M, tag, acc);
+          else if (MT == 4) sk_collect<4, 0>(tpart, c_first, c_last, cstride, M, tag, acc);
+          else if (MT == 8) sk_collect<8, 0>(tpart, c_first, c_last, cstride, M, tag, acc);
           else if (M <= 2) sk_collect<2, 0>(tpart, c_first, c_last, cstride, M, tag, acc);
           else if (M <= 4) sk_collect<4, 0>(tpart, c_first, c_last, cstride, M, tag, acc);
           else if (M <= 8) sk_collect<8, 0>(tpart, c_first, c_last, cstride, M, tag, acc);
@@ -961,7 +964,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         if (!finisher) {
           unsigned long long* pp = tpart + (long long)(cta - c_first) * args.M * kBM;
 #pragma unroll
-          for (int t = 0; t < BN; ++t)
+          for (int t = 0; t < MT; ++t)
             if (t < args.M)
               st_relaxed_u64(pp + (long long)t * kBM,
                              (unsigned long long)__float_as_uint(v[t]) | ((unsigned long long)tag << 32));
@@ -969,9 +972,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
         }
         if (!whole) {
 #pragma unroll
-          for (int t = 0; t < BN; ++t) v[t] = acc[t] + v[t];
+          for (int t = 0; t < MT; ++t) v[t] = acc[t] + v[t];
         }
-        sk_finish<BN>(P, (int)tile, row, v, rs, xch, red, (kPreRes && resid) ? res : nullptr, stage ? slot_s : nullptr,
+        sk_finish<BN, SkPhase, MT>(P, (int)tile, row, v, rs, xch, red, (kPreRes && resid) ? res : nullptr, stage ? slot_s : nullptr,
                       cs_s);
       }
       // phase p done in this CTA: publish (release) for the other CTAs
@@ -1108,13 +1111,23 @@ constexpr int sk_stages() {
 template <int BN, bool DEEP>
 int launch_chain(const ChainMaps& maps, const ChainArgs& a, cudaStream_t st) {
   constexpr int S = sk_stages<BN, DEEP>();
-  auto kern = gemm_chain_kernel<BN, S, DEEP ? 1 : 2>;
+  constexpr int MB = DEEP ? 1 : 2;
+  // token-loop bound: the next power of two >= M (its own instantiation, so
+  // the per-phase epilogue code a small batch executes stays small)
+  int which = 0;
+  auto kern = gemm_chain_kernel<BN, S, MB>;
+  if constexpr (BN == 16) {
+    if (a.M <= 1) kern = gemm_chain_kernel<BN, S, MB, 1>, which = 1;
+    else if (a.M <= 2) kern = gemm_chain_kernel<BN, S, MB, 2>, which = 2;
+    else if (a.M <= 4) kern = gemm_chain_kernel<BN, S, MB, 4>, which = 3;
+    else if (a.M <= 8) kern = gemm_chain_kernel<BN, S, MB, 8>, which = 4;
+  }
   constexpr size_t smem = 1024 + (size_t)S * (kBM * kBK * 2 + BN * kBK * 2) + (2 * S + 4) * 8 + 16 +
                           sk_extra_bytes<BN, DEEP>();
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[5] = {false, false, false, false, false};
+  if (!attr[which]) {
     ASTRAEA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
+    attr[which] = true;
   }
   ASTRAEA_TRY(launch_k(kern, dim3(a.grid), dim3(kThreads), smem, st, maps, a));
   return 0;

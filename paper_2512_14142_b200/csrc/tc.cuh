@@ -200,8 +200,10 @@ __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned l
 }
 
 // Finish one 128-feature tile: thread `row` holds v[t] (t < M) of feature
-// tile*128 + row. All 128 epilogue threads call this together.
-template <int BN, typename A>
+// tile*128 + row. All 128 epilogue threads call this together. MT (<= BN):
+// compile-time bound of the token loops (MT = 1 for a batch of one keeps the
+// code executed per tile small -- it runs once per phase, from a cold cache).
+template <int BN, typename A, int MT = BN>
 __device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* v, const float* rs,
                                           bf16* xch, float* red, const float* res_pre = nullptr,
                                           const int* slot_s = nullptr, const float2* cs_s = nullptr) {
@@ -213,11 +215,11 @@ __device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* 
   const bool fok = f < a.N;
   if (e.ssq_in) {
 #pragma unroll
-    for (int t = 0; t < BN; ++t) v[t] *= rs[t];
+    for (int t = 0; t < MT; ++t) v[t] *= rs[t];
   }
   if (e.kind == EPI_ARGMAX) {
 #pragma unroll
-    for (int t = 0; t < BN; ++t) {
+    for (int t = 0; t < MT; ++t) {
       if (t >= M) break;
       if (a.C && fok) a.C[(long long)t * a.ldc + f] = f2bf(v[t]);
       const unsigned long long k = warp_max64(fok ? argmax_key(v[t], f + e.amax_off) : 0ull);
@@ -228,7 +230,7 @@ __device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* 
   if (e.kind == EPI_NONE || e.kind == EPI_RESIDUAL) {
     float sq[BN];
 #pragma unroll
-    for (int t = 0; t < BN; ++t) {
+    for (int t = 0; t < MT; ++t) {
       sq[t] = 0.f;
       if (t < M && fok) {
         float o = v[t];
@@ -242,7 +244,7 @@ __device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* 
     if (e.ssq_out) {
       const int q = row >> 5, lane = row & 31;
 #pragma unroll
-      for (int t = 0; t < BN; ++t) {
+      for (int t = 0; t < MT; ++t) {
         const float s = warp_sum(sq[t]);
         if (lane == 0) red[q * BN + t] = s;
       }
@@ -255,14 +257,14 @@ __device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* 
   // pair exchange through shared memory (values rounded to bf16, as the
   // unfused formulation materialises them)
 #pragma unroll
-  for (int t = 0; t < BN; ++t) xch[t * kBM + row] = f2bf(v[t]);
+  for (int t = 0; t < MT; ++t) xch[t * kBM + row] = f2bf(v[t]);
   epi_bar();
   if (e.kind == EPI_SILU) {
     if (row >= 64) {
       const int out_f = tile * 64 + (row - 64);
       if (fok) {
 #pragma unroll
-        for (int t = 0; t < BN; ++t)
+        for (int t = 0; t < MT; ++t)
           if (t < M)
             a.C[(long long)t * a.ldc + out_f] = f2bf(silu_rounded(bf2f(xch[t * kBM + row - 64])) * bf2f(xch[t * kBM + row]));
       }
@@ -273,7 +275,7 @@ __device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* 
     const bool rot = head < e.Hq + e.Hkv;
     if (fok) {
 #pragma unroll 4
-      for (int t = 0; t < BN; ++t) {
+      for (int t = 0; t < MT; ++t) {
         if (t >= M) break;
         const float x = bf2f(xch[t * kBM + row]);
         float y = x;
