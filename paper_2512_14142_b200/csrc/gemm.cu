@@ -614,6 +614,7 @@ struct ChainArgs {
   int attn_before[kMaxAttn];   // the GEMM phase that attention k precedes (its output is that phase's A)
   attn::AttnWork at[kMaxAttn];
   int pf_layer;                // >= 0: prefetch that layer's K/V pages into L2 during the last phase
+  int attn_early;              // the first attention's work split runs before griddepcontrol.wait
   SkPhase ph[kMaxPhases];
 };
 constexpr int kAttnCtr = kMaxPhases + 2;   // phase_ctr slots kAttnCtr + k: CTAs done with attention k
@@ -827,6 +828,34 @@ __global__ void __launch_bounds__(kThreads, MINB)
     }
     if (tr && lane == 0) tr[9] = gtimer();
   } else {
+    bool attn0_done = false;
+    if constexpr (kAttn) {
+      if (args.attn_early && args.nattn && args.attn_before[0] == 0) {
+        // The first attention starts before griddepcontrol.wait: its work
+        // split needs only the step's inputs (contexts, block tables); each
+        // warp waits for the previous kernel (q, the new token's K/V, the
+        // workspace epoch) right before its first q / page loads.
+        const int ew = warp - 2;
+        attn::AttnWork aw = args.at[0];
+        auto wait_prev = [&aw, &args](int, int) {
+          pdl_wait();
+          aw.tag = (((unsigned)__ldcg(args.phase_ctr + kMaxPhases + 1) + 1u) << 4) | 8u;
+        };
+        auto done = [](int, int) { asm volatile("fence.proxy.async;" ::: "memory"); };
+        unsigned long long* atr = (tr && ew == 0) ? tr + 16 : nullptr;
+        if (args.attn_kind[0] == 1) attn::attn_cta_phase<128, 4>(aw, cta, G, ew, lane, vs_all, wait_prev, done, atr);
+        else if (args.attn_kind[0] == 2) attn::attn_cta_phase<64, 2>(aw, cta, G, ew, lane, vs_all, wait_prev, done);
+        else attn::attn_cta_phase<64, 4>(aw, cta, G, ew, lane, vs_all, wait_prev, done);
+        pdl_wait();
+        asm volatile("fence.proxy.async;" ::: "memory");
+        epi_bar();
+        if (threadIdx.x == 64) {
+          atom_add_acq_rel(args.phase_ctr + kAttnCtr, 1);
+          if (tr) tr[15] = gtimer();   // this CTA's share of attention 0 written
+        }
+        attn0_done = true;
+      }
+    }
     pdl_wait();
     const int epoch = __ldcg(args.phase_ctr + kMaxPhases + 1) + 1;   // launches completed on this workspace + 1
     const int quarter = warp & 3;
@@ -847,7 +876,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         epi_bar();
       }
       if constexpr (kAttn) {
-        for (int k = 0; k < args.nattn; ++k) {
+        for (int k = attn0_done ? 1 : 0; k < args.nattn; ++k) {
           if (args.attn_before[k] != p) continue;
           // A layer's paged decode attention (attn_mma.cuh), by this CTA's
           // epilogue warps, while warp 0 already streams phase p's weight
@@ -1367,6 +1396,11 @@ static int run_chain(int M, int nph, const astraea_gemm_phase* ph, void* ws, siz
     a.pf_layer = (pf && at->layer + 1 < g.num_layers) ? at->layer + 1 : -1;
   }
   a.nattn = nattn;
+  static const int attn_early = [] {
+    const char* e = getenv("ASTRAEA_CHAIN_ATTN_EARLY");
+    return e ? atoi(e) : 1;
+  }();
+  a.attn_early = attn_early;
   a.M = M;
   a.grid = num_sms();
   a.nph = nph;
