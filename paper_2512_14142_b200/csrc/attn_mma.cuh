@@ -231,60 +231,139 @@ struct AttnWork {
   int M;
 };
 
-// One layer's attention by the 4 epilogue warps of every CTA. The (row, kv
-// head) sequences' pages are split evenly over the CTAs; inside a CTA the
-// four warps take every fourth page of the CTA's piece and merge in shared
-// memory, so each sequence has at most one partial per CTA. The last CTA to
-// finish a split sequence merges the partials (CTA order: deterministic); the
-// kv head's flag is raised when all M rows of that head are written.
-// L2 prefetch of the K/V pages this warp will read in attn_cta_phase (same
-// work distribution): issued ahead -- e.g. by the previous layer's launch --
-// so the attention's page loads hit L2.
-template <int D>
-__device__ __forceinline__ void attn_cta_prefetch(const AttnWork& A, int cta, int grid, int warp, int lane) {
-  const int M = A.M, Hkv = A.Hkv;
-  // pages per row (retired rows count one empty page so that every (row, head) is written)
-  int pg0 = 0, pg1 = 0;
-  if (lane < M) pg0 = max(1, (__ldg(A.ctx + lane) + kAttnBT - 1) / kAttnBT);
-  if (lane + 32 < M) pg1 = max(1, (__ldg(A.ctx + lane + 32) + kAttnBT - 1) / kAttnBT);
-  int s0 = pg0, s1 = pg1;   // inclusive scan over rows 0..63 (lane holds rows lane and lane+32)
+// Work split of one layer's attention over the CTAs (every lane of a warp
+// computes the same result). A (row, kv head) sequence has pg pages (retired
+// rows count one empty page, so every output row is written).
+//  * aligned (sequences <= CTAs): each sequence is cut into ceil(pg / qc)
+//    parts of qc consecutive pages on consecutive CTAs, one part per CTA;
+//    qc >= 4 * min_pages, <= 32 parts per sequence, the smallest qc (from the
+//    even share up) whose parts fit the grid. No CTA works on two sequences,
+//    so no piece waits behind another.
+//  * contiguous (more sequences than CTAs): the concatenated pages are cut
+//    into equal ranges of qc pages; a CTA walks the pieces of its range.
+// A piece = (row b, head h, pages [pa, pb)); its sequence's parts live on
+// CTAs first_c..last_c, first_c merges.
+struct AttnPiece {
+  int b, h, pa, pb, first_c, last_c;
+};
+
+__device__ __forceinline__ int warp_sum_int(int v) {
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int a = __shfl_up_sync(0xffffffffu, s0, o), c = __shfl_up_sync(0xffffffffu, s1, o);
-    if (lane >= o) {
-      s0 += a;
-      s1 += c;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+struct AttnSplit {
+  const AttnWork* A;
+  int lane, cta;
+  bool aligned;
+  int qc, my0, my1;       // contiguous: this CTA's page range
+  int pg0, pg1;           // pages of rows lane, lane + 32
+  int ex0, ex1;           // exclusive prefixes: pages (contiguous) or parts (aligned) of rows lane, lane + 32
+  int np0, np1;           // aligned: parts of rows lane, lane + 32
+  int n_pieces;           // this CTA's pieces (aligned: 0 or 1)
+  int cur;                // contiguous: next page of the range
+
+  __device__ __forceinline__ void init(const AttnWork& W, int cta_, int grid, int lane_) {
+    A = &W;
+    lane = lane_;
+    cta = cta_;
+    const int M = W.M, Hkv = W.Hkv;
+    pg0 = pg1 = 0;
+    if (lane < M) pg0 = max(1, (__ldg(W.ctx + lane) + kAttnBT - 1) / kAttnBT);
+    if (lane + 32 < M) pg1 = max(1, (__ldg(W.ctx + lane + 32) + kAttnBT - 1) / kAttnBT);
+    const int total = warp_sum_int(pg0 + pg1);
+    const int maxpg = warp_max_int(max(pg0, pg1));
+    qc = max(max(4 * W.min_pages, (Hkv * total + grid - 1) / grid), (maxpg + 31) / 32);
+    aligned = Hkv * M <= grid;
+    int v0 = pg0, v1 = pg1;
+    if (aligned) {
+      for (int it = 0; it < 64; ++it) {
+        np0 = (pg0 + qc - 1) / qc;
+        np1 = (pg1 + qc - 1) / qc;
+        if (Hkv * warp_sum_int(np0 + np1) <= grid) break;
+        qc += max(1, qc / 8);
+      }
+      v0 = np0;
+      v1 = np1;
+    }
+    int s0 = v0, s1 = v1;   // inclusive scan over rows 0..63
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int x = __shfl_up_sync(0xffffffffu, s0, o), y = __shfl_up_sync(0xffffffffu, s1, o);
+      if (lane >= o) {
+        s0 += x;
+        s1 += y;
+      }
+    }
+    s1 += __shfl_sync(0xffffffffu, s0, 31);
+    ex0 = s0 - v0;
+    ex1 = s1 - v1;
+    const int all = Hkv * __shfl_sync(0xffffffffu, s1, 31);
+    if (aligned) {
+      n_pieces = cta < all ? 1 : 0;
+    } else {
+      my0 = cta * qc;
+      my1 = min(all, my0 + qc);
+      cur = my0;
+      n_pieces = my0 < my1 ? 1 : 0;   // at least one; next() tells when the range ends
     }
   }
-  s1 += __shfl_sync(0xffffffffu, s0, 31);
-  const int total_pages = __shfl_sync(0xffffffffu, s1, 31);
-  const int U = Hkv * total_pages;
-  // pages per CTA: cover the SMs, >= 4 * min_pages, <= 32 parts per sequence
-  const int maxpg = warp_max_int(max(pg0, pg1));
-  const int qc = max(max(4 * A.min_pages, (U + grid - 1) / grid), (maxpg + 30) / 31);
-  const int my0 = cta * qc, my1 = min(U, my0 + qc);
-  const int ex0 = s0 - pg0, ex1 = s1 - pg1;   // exclusive prefixes of rows lane, lane+32
-  auto resolve = [&](int cur, int& b, int& h, int& seq0, int& seq1, int& pe) {
-    const unsigned b0 = __ballot_sync(0xffffffffu, lane < M && Hkv * ex0 <= cur);
-    const unsigned b1 = __ballot_sync(0xffffffffu, lane + 32 < M && Hkv * ex1 <= cur);
-    b = __popc(b0) + __popc(b1) - 1;
-    const int exb = __shfl_sync(0xffffffffu, b < 32 ? ex0 : ex1, b & 31);
-    const int pgb = __shfl_sync(0xffffffffu, b < 32 ? pg0 : pg1, b & 31);
-    const int row_start = Hkv * exb;
-    h = (cur - row_start) / pgb;
-    seq0 = row_start + h * pgb;
-    seq1 = seq0 + pgb;
-    pe = min(my1, seq1);
-  };
-  // L2 prefetch of this warp's K/V pages before waiting for the QKV flags
-  for (int cur = my0; cur < my1;) {
-    int b, h, seq0, seq1, pe;
-    resolve(cur, b, h, seq0, seq1, pe);
-    const int ctx_b = __ldg(A.ctx + b);
-    const int32_t* trow = A.table + (long long)b * A.max_blocks;
-    const long long k_off = ((long long)(A.layer * 2) * A.Hkv + h) * kAttnBT * D;
-    const long long v_off = ((long long)(A.layer * 2 + 1) * A.Hkv + h) * kAttnBT * D;
-    for (int p = cur - seq0 + warp + 4 * lane; p < pe - seq0; p += 128) {
+  // the row whose prefix (in units of one head) covers position x
+  __device__ __forceinline__ int row_of(int x, int& ex, int& pg, int& np) const {
+    const int Hkv = A->Hkv, M = A->M;
+    const unsigned b0 = __ballot_sync(0xffffffffu, lane < M && Hkv * ex0 <= x);
+    const unsigned b1 = __ballot_sync(0xffffffffu, lane + 32 < M && Hkv * ex1 <= x);
+    const int b = max(0, __popc(b0) + __popc(b1) - 1);
+    ex = __shfl_sync(0xffffffffu, b < 32 ? ex0 : ex1, b & 31);
+    pg = __shfl_sync(0xffffffffu, b < 32 ? pg0 : pg1, b & 31);
+    np = aligned ? __shfl_sync(0xffffffffu, b < 32 ? np0 : np1, b & 31) : 0;
+    return b;
+  }
+  // the piece starting at the current position; false when the CTA is done
+  __device__ __forceinline__ bool next(AttnPiece& pc) {
+    const int Hkv = A->Hkv;
+    int ex, pg, np;
+    if (aligned) {
+      if (n_pieces == 0) return false;
+      n_pieces = 0;
+      pc.b = row_of(cta, ex, pg, np);
+      np = max(1, np);
+      const int r0 = cta - Hkv * ex, part = r0 % np;
+      pc.h = r0 / np;
+      pc.pa = part * qc;
+      pc.pb = min(pg, pc.pa + qc);
+      pc.first_c = cta - part;
+      pc.last_c = pc.first_c + np - 1;
+      return true;
+    }
+    if (cur >= my1) return false;
+    pc.b = row_of(cur, ex, pg, np);
+    const int row_start = Hkv * ex;
+    pc.h = (cur - row_start) / pg;
+    const int seq0 = row_start + pc.h * pg, seq1 = seq0 + pg, pe = min(my1, seq1);
+    pc.pa = cur - seq0;
+    pc.pb = pe - seq0;
+    pc.first_c = seq0 / qc;
+    pc.last_c = (seq1 - 1) / qc;
+    cur = pe;
+    return true;
+  }
+};
+
+// L2 prefetch of the K/V pages this CTA's warps read in attn_cta_phase (same
+// work split), e.g. issued by the previous layer's launch.
+template <int D>
+__device__ __forceinline__ void attn_cta_prefetch(const AttnWork& A, int cta, int grid, int warp, int lane) {
+  AttnSplit sp;
+  sp.init(A, cta, grid, lane);
+  AttnPiece pc;
+  while (sp.next(pc)) {
+    const int ctx_b = __ldg(A.ctx + pc.b);
+    const int32_t* trow = A.table + (long long)pc.b * A.max_blocks;
+    const long long k_off = ((long long)(A.layer * 2) * A.Hkv + pc.h) * kAttnBT * D;
+    const long long v_off = ((long long)(A.layer * 2 + 1) * A.Hkv + pc.h) * kAttnBT * D;
+    for (int p = pc.pa + warp + 4 * lane; p < pc.pb; p += 128) {
       const int blk = p * kAttnBT < ctx_b ? __ldg(trow + p) : -1;
       if (blk >= 0) {
         const bf16* page = A.pool + (long long)blk * A.block_el;
@@ -292,99 +371,52 @@ __device__ __forceinline__ void attn_cta_prefetch(const AttnWork& A, int cta, in
         l2_prefetch_bulk(page + v_off, kAttnBT * D * 2);
       }
     }
-    cur = pe;
   }
 }
 
+// One layer's attention by the 4 epilogue warps of every CTA: this CTA's
+// piece (attn_split) -- the four warps take every fourth page and merge in
+// shared memory; a split sequence's part-0 CTA merges the other parts'
+// self-validating partials (CTA order: deterministic) and writes the output.
+// wait_head(h, lane) runs before the first q / page load (e.g. waits for the
+// kernel that produced q and the new K/V); done_head(h, thread) after the
+// merged output is written.
 template <int D, int G, class WaitHead, class DoneHead>
 __device__ __forceinline__ void attn_cta_phase(const AttnWork& A, int cta, int grid, int warp, int lane,
                                                bf16* vs_all, const WaitHead& wait_head, const DoneHead& done_head,
                                                unsigned long long* atr = nullptr) {
-  // atr (diagnostics, may be null): this warp's first piece: [0] entry,
-  // [1] q/k/v flags seen, [2] q loaded, [3] pages done, [4] CTA merge +
-  // partial published, [5] split merge done, [6] output published, [7] exit
-  auto mark = [&](int k, bool first) {
-    if (atr && first && lane == 0) atr[k] = gtimer_();
+  // atr (diagnostics, may be null): [0] entry, [1] wait_head passed, [2] q
+  // loaded, [3] pages done, [4] CTA merge + partial published, [5] split
+  // merge done, [6] output published, [7] exit, [8..12] first page, [13]
+  // merger: all parts seen, [14] merger: spins
+  auto mark = [&](int k) {
+    if (atr && lane == 0) atr[k] = gtimer_();
   };
-  mark(0, true);
-  const int M = A.M, Hkv = A.Hkv;
+  mark(0);
   const int et = warp * 32 + lane;
   bf16* vs = vs_all + warp * (kAttnWarpBytes / 2);
-  // pages per row (retired rows count one empty page so that every (row, head) is written)
-  int pg0 = 0, pg1 = 0;
-  if (lane < M) pg0 = max(1, (__ldg(A.ctx + lane) + kAttnBT - 1) / kAttnBT);
-  if (lane + 32 < M) pg1 = max(1, (__ldg(A.ctx + lane + 32) + kAttnBT - 1) / kAttnBT);
-  int s0 = pg0, s1 = pg1;   // inclusive scan over rows 0..63 (lane holds rows lane and lane+32)
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int a = __shfl_up_sync(0xffffffffu, s0, o), c = __shfl_up_sync(0xffffffffu, s1, o);
-    if (lane >= o) {
-      s0 += a;
-      s1 += c;
-    }
-  }
-  s1 += __shfl_sync(0xffffffffu, s0, 31);
-  const int total_pages = __shfl_sync(0xffffffffu, s1, 31);
-  const int U = Hkv * total_pages;
-  // pages per CTA: cover the SMs, >= 4 * min_pages, <= 32 parts per sequence
-  const int maxpg = warp_max_int(max(pg0, pg1));
-  const int qc = max(max(4 * A.min_pages, (U + grid - 1) / grid), (maxpg + 30) / 31);
-  const int my0 = cta * qc, my1 = min(U, my0 + qc);
-  const int ex0 = s0 - pg0, ex1 = s1 - pg1;   // exclusive prefixes of rows lane, lane+32
-  auto resolve = [&](int cur, int& b, int& h, int& seq0, int& seq1, int& pe) {
-    const unsigned b0 = __ballot_sync(0xffffffffu, lane < M && Hkv * ex0 <= cur);
-    const unsigned b1 = __ballot_sync(0xffffffffu, lane + 32 < M && Hkv * ex1 <= cur);
-    b = __popc(b0) + __popc(b1) - 1;
-    const int exb = __shfl_sync(0xffffffffu, b < 32 ? ex0 : ex1, b & 31);
-    const int pgb = __shfl_sync(0xffffffffu, b < 32 ? pg0 : pg1, b & 31);
-    const int row_start = Hkv * exb;
-    h = (cur - row_start) / pgb;
-    seq0 = row_start + h * pgb;
-    seq1 = seq0 + pgb;
-    pe = min(my1, seq1);
-  };
-  // L2 prefetch of this warp's K/V pages before waiting for the QKV flags
-  if (A.prefetch) {
-  for (int cur = my0; cur < my1;) {
-    int b, h, seq0, seq1, pe;
-    resolve(cur, b, h, seq0, seq1, pe);
-    const int ctx_b = __ldg(A.ctx + b);
-    const int32_t* trow = A.table + (long long)b * A.max_blocks;
-    const long long k_off = ((long long)(A.layer * 2) * A.Hkv + h) * kAttnBT * D;
-    const long long v_off = ((long long)(A.layer * 2 + 1) * A.Hkv + h) * kAttnBT * D;
-    for (int p = cur - seq0 + warp + 4 * lane; p < pe - seq0; p += 128) {
-      const int blk = p * kAttnBT < ctx_b ? __ldg(trow + p) : -1;
-      if (blk >= 0) {
-        const bf16* page = A.pool + (long long)blk * A.block_el;
-        l2_prefetch_bulk(page + k_off, kAttnBT * D * 2);
-        l2_prefetch_bulk(page + v_off, kAttnBT * D * 2);
-      }
-    }
-    cur = pe;
-  }
-  }
+  AttnSplit sp;
+  sp.init(A, cta, grid, lane);
   constexpr int EPT = (G * D + 128 - 1) / 128;   // merged elements per thread
   unsigned heads_ready = 0;
-  for (int cur = my0; cur < my1;) {
-    int b, h, seq0, seq1, pe;
-    resolve(cur, b, h, seq0, seq1, pe);
-    const int pa = cur - seq0, pb = pe - seq0;
-    const bool first_piece = cur == my0;
+  AttnPiece pc;
+  while (sp.next(pc)) {
+    const int b = pc.b, h = pc.h;
     if (!(heads_ready >> h & 1)) {
       wait_head(h, lane);
       heads_ready |= 1u << h;
     }
-    mark(1, first_piece);
+    mark(1);
     const int ctx_b = __ldg(A.ctx + b);
     const int r8 = lane >> 2, quad = lane & 3;
     uint32_t qa[D / 8];
     attn_load_q<D>(A.q + (long long)b * A.q_stride + (long long)(h * G + r8) * D, r8 < G, quad, qa);
-    mark(2, first_piece);
+    mark(2);
     AttnAcc<D> st;
     const PageSrc src = page_src<D>(A.pool, A.block_el, A.layer, A.Hkv, h, A.table + (long long)b * A.max_blocks,
                                     A.scale_log2);
-    attn_pages<D>(src, pa + warp, pb, 4, ctx_b, qa, vs, st, lane, (atr && first_piece) ? atr + 8 : nullptr);
-    mark(3, first_piece);
+    attn_pages<D>(src, pc.pa + warp, pc.pb, 4, ctx_b, qa, vs, st, lane, atr ? atr + 8 : nullptr);
+    mark(3);
     // ---- CTA merge of the 4 warps' states (warp order) through shared memory
     float* wst = reinterpret_cast<float*>(vs);   // this warp's V page is free now: [G] m, [G] l, [G][D] o
     __syncwarp();
@@ -417,16 +449,13 @@ __device__ __forceinline__ void attn_cta_phase(const AttnWork& A, int cta, int g
         }
       }
     }
-    // Split sequences: the CTA owning the sequence's first pages merges. Its
-    // piece closes its range, while the other parts open the ranges of the
-    // following CTAs, so they are normally published first; parts are
-    // self-validating 64-bit words (fp32 bits | tag << 32) -- one round trip,
-    // no arrival counter. Merge order: own part, then the CTAs in order.
-    const int first_c = seq0 / qc, last_c = (seq1 - 1) / qc;
+    // Split sequences: part 0's CTA merges. Parts are self-validating 64-bit
+    // words (fp32 bits | tag << 32) -- one round trip, no arrival counter.
+    // Merge order: own part, then the CTAs in order.
+    const int first_c = pc.first_c, last_c = pc.last_c;
     const bool merger = cta == first_c;
     bool done = first_c == last_c;
     if (!done && !merger) {
-      // contributor: this piece opens this CTA's range (slot 0)
       unsigned long long* part = A.ws + (long long)cta * G * (D + 2);
 #pragma unroll
       for (int e = 0; e < EPT; ++e) {
@@ -439,7 +468,7 @@ __device__ __forceinline__ void attn_cta_phase(const AttnWork& A, int cta, int g
           }
         }
       }
-      mark(4, first_piece);
+      mark(4);
     } else if (!done) {
       // a thread's EPT elements lie in one head row g: per part, m and l are
       // two words and o is EPT words; eight parts are polled together
@@ -467,12 +496,12 @@ __device__ __forceinline__ void attn_cta_phase(const AttnWork& A, int cta, int g
             for (int e = 0; e < EPT; ++e) ready &= (unsigned)(po[k][e] >> 32) == A.tag;
           }
           if (ready) {
-            if (atr && lane == 0 && first_piece && c0 == first_c + 1) atr[14] = (unsigned long long)spin;
+            if (atr && lane == 0 && c0 == first_c + 1) atr[14] = (unsigned long long)spin;
             break;
           }
           __nanosleep(64);
         }
-        if (atr && first_piece && c0 == first_c + 1) {
+        if (atr && c0 == first_c + 1) {
           __syncwarp();
           if (lane == 0) atr[13] = gtimer_();   // every lane of the warp has its words
         }
@@ -497,7 +526,7 @@ __device__ __forceinline__ void attn_cta_phase(const AttnWork& A, int cta, int g
         }
       }
       done = true;
-      mark(5, first_piece);
+      mark(5);
     }
     if (done) {
       bf16* out = A.out + (long long)b * (A.Hq * D) + (long long)h * G * D;
@@ -508,11 +537,10 @@ __device__ __forceinline__ void attn_cta_phase(const AttnWork& A, int cta, int g
       }
       done_head(h, warp * 32 + lane);   // all 128 threads
     }
-    mark(6, first_piece);
+    mark(6);
     epi_bar();   // the warps' shared-memory states are rewritten by the next piece
-    cur = pe;
   }
-  mark(7, true);
+  mark(7);
 }
 
 }  // namespace attn
