@@ -307,9 +307,16 @@ def main():
     d2h = (dp.stats["d2h_bytes"] - s0["d2h_bytes"]) // args.steps
 
     # ---- measured-clock JCT (same scheduler, B200 durations, virtual API waits)
-    pol, mem, scfg = make_run(host, shard, pred, args, cfg.kv_bytes_per_token)
-    mrep = GpuEngine(shard, pol, pred, mem, scfg, dp, clock="measured").run()
-    agg = mrep.aggregates()
+    # three runs, median by avg JCT: the measured-clock schedule reacts to
+    # run-to-run timing noise (an arrival before or after a batch boundary
+    # changes later decisions), so one run can sit +-30% from another
+    mruns = []
+    for _ in range(3):
+        pol, mem, scfg = make_run(host, shard, pred, args, cfg.kv_bytes_per_token)
+        r_ = GpuEngine(shard, pol, pred, mem, scfg, dp, clock="measured").run()
+        mruns.append((r_.aggregates(), r_.requests_per_second()))
+    mruns.sort(key=lambda x: x[0]["avg_jct"])
+    agg, m_rps = mruns[1]
 
     # ---- dominant kernel: one decoder layer's fused launch (paged attention ->
     # O -> gate/up -> down -> next QKV in one persistent tcgen05 kernel) at the
@@ -345,8 +352,8 @@ def main():
                                f"tcgen05 stream-K), M={B}, ctx={chain_ctx}",
                      "algorithmic_bytes_per_launch": chain_bytes, "launch_ms": chain_ms,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, copy burst)"},
-        "jct_measured_clock": {"avg_s": agg["avg_jct"], "p99_s": agg["p99_jct"],
-                               "req_per_s": mrep.requests_per_second()},
+        "jct_measured_clock": {"avg_s": agg["avg_jct"], "p99_s": agg["p99_jct"], "req_per_s": m_rps,
+                               "runs_avg_s": [r[0]["avg_jct"] for r in mruns], "note": "median of 3 runs"},
         "decode_step": {"batch": B, "ms": step_ms, "hbm_gbs": step_gbs, "frac": step_gbs / hbm},
         "kv_swap": swap,
         "kv_decisions": {k: v for k, v in json.loads(ref_rep.to_json())["audits"].items() if k == "events_processed"},
