@@ -1132,9 +1132,12 @@ constexpr size_t sk_extra_bytes() {
 // Single GEMMs: ~104 KB so two CTAs fit per SM and the next kernel's CTA can
 // become resident and prefetch its weights (PDL) while this one drains.
 // Chains: one deep ring per SM (~200 KB), the phases hide each other's tails.
+#ifndef ASTRAEA_DEEP_RING_KB
+#define ASTRAEA_DEEP_RING_KB 200   // smem budget of a deep chain's ring + extras (KB)
+#endif
 template <int BN, bool DEEP>
 constexpr int sk_stages() {
-  return (int)(((DEEP ? 200 : 104) * 1024 - sk_extra_bytes<BN, DEEP>()) / (kBM * kBK * 2 + BN * kBK * 2));
+  return (int)(((DEEP ? ASTRAEA_DEEP_RING_KB : 104) * 1024 - sk_extra_bytes<BN, DEEP>()) / (kBM * kBK * 2 + BN * kBK * 2));
 }
 
 template <int BN, bool DEEP>
