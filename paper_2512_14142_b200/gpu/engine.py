@@ -16,7 +16,11 @@ Clock modes
   ``measured``  the clock advances by CUDA-event durations of each member's
                 segment (batch start -> the decode step that retires it) and
                 of each swap; API waits stay virtual. This gives JCT and req/s
-                of the B200 data path under the same scheduler.
+                of the B200 data path under the same scheduler. Swaps share
+                one host link: they complete in issue order, each after the
+                previous one (a FIFO channel -- SPEC.md:323 promises it, the
+                reference's independent delays lack it),
+                exactly as the data path runs them on its one swap stream.
 """
 
 from __future__ import annotations
@@ -37,6 +41,7 @@ class GpuEngine(Engine):
         self.clock = clock
         self.datapath = datapath
         self.device_audit = device_audit
+        self._link_free = 0.0   # measured clock: when the host link finishes its queued swaps
 
     def _launch_batch(self, members):
         measured = self.datapath.launch_batch(members)
@@ -44,7 +49,10 @@ class GpuEngine(Engine):
 
     def _swap_delay(self, state, direction):
         if self.clock == "measured":
-            return self.datapath.swap_seconds(state, direction)
+            # FIFO host link: this transfer starts when the previous one ends
+            start = max(self.now, self._link_free)
+            self._link_free = start + self.datapath.swap_seconds(state, direction)
+            return self._link_free - self.now
         return super()._swap_delay(state, direction)
 
     def _try_start_batch(self):
