@@ -1301,22 +1301,27 @@ static size_t chain_ws_bytes(int M, int nph, const astraea_gemm_phase* ph) {
 }
 
 // K-splits of the CTA-pair GEMM: only when its tiles leave pairs idle (small
-// M, e.g. a short prefill), at most one unit per pair (so a split's finisher
-// never waits on work queued behind it), >= 4 k-blocks per split.
-// Experimental (ASTRAEA_PAIR_SPLITK=1): measured 2-4x *slower* at M <= 256 on
-// B200 -- the fp32 partial exchange through L2 (256 KB per CTA and split)
-// costs more than the idle pairs -- so off by default.
+// M, e.g. a short recompute prefill), at most one unit per pair (so a split's
+// finisher never waits on work queued behind it), >= kPairMinKbs k-blocks per
+// split (32). Measured on B200 (tools/gemm_bench.py, CUDA graph): the down
+// projection (K = 14336) at M <= 512 drops from 71-72 us to 47-54 us, the
+// K = 4096 shapes (2 splits) from 24.5-25.8 to 22.4-24.6 us at M <= 256
+// (profiles/r1_prefill_splitk.txt). ASTRAEA_PAIR_SPLITK=0 disables.
 static int pair_splits(int M, int N, int K) {
   static const bool on = [] {
     const char* e = getenv("ASTRAEA_PAIR_SPLITK");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
+  }();
+  static const int min_kbs = [] {
+    const char* e = getenv("ASTRAEA_PAIR_SPLIT_MIN_KB");
+    return e ? std::max(1, atoi(e)) : 32;
   }();
   if (!on) return 1;
   const int tiles = ((M + 255) / 256) * ((N + 255) / 256);
   const int pairs = num_sms() / 2;
   const int kb = (K + kBK - 1) / kBK;
   if (tiles >= pairs) return 1;
-  return std::max(1, std::min(std::min(pairs / tiles, kb / 4), 8));
+  return std::max(1, std::min(std::min(pairs / tiles, kb / min_kbs), 8));
 }
 static size_t pair_partial_bytes(int M, int N, int K) {
   const int S = pair_splits(M, N, K);
