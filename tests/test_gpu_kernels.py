@@ -473,3 +473,51 @@ def test_row_ssq_matches_torch():
     torch.cuda.synchronize()
     ref = x.float().view(37, 32, 128).pow(2).sum(-1).T
     assert s.shape == (32, 37) and torch.allclose(s, ref, rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.parametrize("Hq,Hkv,D", [(32, 8, 128), (8, 4, 64), (16, 4, 64)])
+@pytest.mark.parametrize("ctxs", [[1], [900], [1, 16, 17, 300], [2316, 5, 0, 1000, 64],
+                                  [37 * (b % 7) + 1 for b in range(24)], [8000, 3]])
+def test_fused_chain_attention_matches_oracle(Hq, Hkv, D, ctxs):
+    """The decode attention run as the chain's first phase (aligned split when
+    the (row, kv head) sequences fit the grid, contiguous page ranges when
+    they do not -- 24 rows x 8 heads) against the fp32 oracle; the chained
+    GEMM consumes exactly what the attention wrote; twice on one workspace
+    (launch epochs, counter resets)."""
+    Lyr = 2
+    B = len(ctxs)
+    max_blocks = max(1, max((c + 15) // 16 for c in ctxs))
+    nb = B * max_blocks + 3
+    pool, geo = make_pool(nb, Lyr, Hkv, D, seed=B + D)
+    perm = torch.randperm(nb, generator=torch.Generator().manual_seed(B))[: B * max_blocks].view(B, max_blocks).int()
+    table = perm.clone()
+    for b, c in enumerate(ctxs):
+        table[b, (c + 15) // 16:] = -1
+    g = torch.Generator(device=DEV).manual_seed(11)
+    stride = (Hq + 2 * Hkv) * D
+    qkv = torch.randn(B, stride, generator=g, device=DEV).bfloat16()
+    N = 256
+    wo = (torch.randn(N, Hq * D, generator=g, device=DEV) * 0.05).bfloat16()
+    scale = 1 / math.sqrt(D)
+    ctx_d = torch.tensor(ctxs, dtype=torch.int32, device=DEV)
+    table_d = table.to(DEV)
+    ws = torch.zeros(64 << 20, dtype=torch.float32, device=DEV)
+    ref = attention_ref.decode_ref(pool.cpu(), 1, qkv[:, : Hq * D].view(B, Hq, D).cpu(), table, ctxs, scale,
+                                   Lyr, Hkv, D)
+    for rep in range(2):
+        att = torch.full((B, Hq * D), float("nan"), dtype=torch.bfloat16, device=DEV)
+        y = torch.empty(B, N, dtype=torch.bfloat16, device=DEV)
+        attn = dict(pool=pool, geo=geo, layer=1, num_q_heads=Hq, q=qkv, q_stride=stride, table=table_d,
+                    ctx=ctx_d, scale=scale, out=att)
+        ops.gemm_chain([dict(a=att, w=wo, out=y)], ws, attn=attn)
+        torch.cuda.synchronize()
+        got = att.view(B, Hq, D).cpu().float()
+        for b, c in enumerate(ctxs):
+            if c == 0:
+                assert torch.count_nonzero(got[b]) == 0, (rep, b)
+            else:
+                assert rel_err(got[b], ref[b]) < 1e-2, (rep, b, c)
+        y_ref = torch.empty_like(y)
+        ops.gemm_ex(att, wo, y_ref, workspace=ws)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y_ref), rep
