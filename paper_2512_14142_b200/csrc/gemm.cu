@@ -730,6 +730,14 @@ __global__ void __launch_bounds__(kThreads, MINB)
         const int KB = P.kbs;
         long long u0, u1;
         sk_range(P, cta, u0, u1);
+        // nothing to load: no counter wait either (the last phase's counter
+        // may be reset for the next launch as soon as every epilogue has
+        // arrived) -- but griddepcontrol.wait still comes first, before this
+        // thread reads any counter of a later phase
+        if (u0 == u1) {
+          if (p == 0) pdl_wait();
+          continue;
+        }
         const int pre = (int)(u1 - u0 < STAGES ? u1 - u0 : STAGES);
         // weights first: independent of the previous phase / kernel
         for (int k = 0; k < pre; ++k) {
@@ -1006,26 +1014,27 @@ __global__ void __launch_bounds__(kThreads, MINB)
         sk_finish<BN, SkPhase, MT>(P, (int)tile, row, v, rs, xch, red, (kPreRes && resid) ? res : nullptr, stage ? slot_s : nullptr,
                       cs_s);
       }
-      // phase p done in this CTA: publish (release) for the other CTAs
+      // phase p done in this CTA: publish (release) for the other CTAs. The
+      // last CTA to finish the last phase resets the counters for the next
+      // launch: every CTA has passed all of its counter waits by then (its
+      // producer waited before loading this phase's activations), and the
+      // next launch touches them only after griddepcontrol.wait.
       epi_bar();
       if (threadIdx.x == 64) {
-        atom_add_acq_rel(args.phase_ctr + p, 1);
+        const int before = atom_add_acq_rel(args.phase_ctr + p, 1);
         if (tr && p < 4) tr[5 + p] = gtimer();
+        if (p == args.nph - 1 && before == G - 1) {
+          for (int q = 0; q <= kMaxPhases; ++q) args.phase_ctr[q] = 0;
+          for (int k = 0; k < kMaxAttn; ++k) args.phase_ctr[kAttnCtr + k] = 0;
+          args.phase_ctr[kMaxPhases + 1] += 1;   // launch epoch (tags of the stream-K partials)
+        }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
-  if (threadIdx.x == 0) {
-    // the last CTA to leave resets the phase counters for the next launch
-    if (atom_add_acq_rel(args.phase_ctr + kMaxPhases, 1) == G - 1) {
-      for (int p = 0; p <= kMaxPhases; ++p) args.phase_ctr[p] = 0;
-      for (int k = 0; k < kMaxAttn; ++k) args.phase_ctr[kAttnCtr + k] = 0;
-      args.phase_ctr[kMaxPhases + 1] += 1;   // launch epoch (tags of the stream-K partials)
-    }
-    if (tr) tr[10] = gtimer();
-  }
+  if (tr && threadIdx.x == 0) tr[10] = gtimer();
 }
 
 __global__ void rope_table_kernel(const int32_t* __restrict__ pos, int T, int half, float theta,
