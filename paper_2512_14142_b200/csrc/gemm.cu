@@ -500,10 +500,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + buf * 256;
       mbar_wait(&tfull[buf], (lt >> 1) & 1);
       tc_fence_after();
-      if (sp > 0) {
+      if (sp < S - 1) {
         // contributor: publish this split's accumulator rows as tagged partials
         unsigned long long* p =
-            args.part + (((long long)t * (S - 1) + (sp - 1)) * 2 + rank) * kPartCta + row_local;
+            args.part + (((long long)t * (S - 1) + sp) * 2 + rank) * kPartCta + row_local;
         for (int c = 0; c < 8; ++c) {
           float v[32];
           tmem_ld32(taddr + c * 32, v);
@@ -1309,13 +1309,16 @@ static size_t chain_ws_bytes(int M, int nph, const astraea_gemm_phase* ph) {
   return kHeadBytes + part;
 }
 
-// K-splits of the CTA-pair GEMM: only when its tiles leave pairs idle (small
-// M, e.g. a short recompute prefill), at most one unit per pair (so a split's
-// finisher never waits on work queued behind it), >= kPairMinKbs k-blocks per
-// split (32). Measured on B200 (tools/gemm_bench.py, CUDA graph): the down
-// projection (K = 14336) at M <= 512 drops from 71-72 us to 47-54 us, the
-// K = 4096 shapes (2 splits) from 24.5-25.8 to 22.4-24.6 us at M <= 256
-// (profiles/r1_prefill_splitk.txt). ASTRAEA_PAIR_SPLITK=0 disables.
+// K-splits of the CTA-pair GEMM (units = tiles x splits, dealt round-robin
+// to the pairs; the last split of a tile finishes it, so its contributors
+// come earlier on every pair). Only when the tiles leave pairs idle (small
+// M, e.g. a short recompute prefill): at most pairs / tiles splits, >= 32
+// k-blocks each. Measured on B200 (tools/gemm_bench.py, CUDA graph,
+// profiles/r1_prefill_splitk.txt): the down projection at M <= 512 drops
+// from 71-72 us to 47-54 us, the K = 4096 shapes at M <= 256 from 24.5-26
+// to 22.7-24.7 us; splitting when tiles >= pairs is 1.2-4x slower (the fp32
+// partial exchange through L2 outweighs the balance). ASTRAEA_PAIR_SPLITK=0
+// disables, ASTRAEA_PAIR_SPLITS forces S (experiments).
 static int pair_splits(int M, int N, int K) {
   static const bool on = [] {
     const char* e = getenv("ASTRAEA_PAIR_SPLITK");
@@ -1325,10 +1328,15 @@ static int pair_splits(int M, int N, int K) {
     const char* e = getenv("ASTRAEA_PAIR_SPLIT_MIN_KB");
     return e ? std::max(1, atoi(e)) : 32;
   }();
+  static const int forced = [] {
+    const char* e = getenv("ASTRAEA_PAIR_SPLITS");
+    return e ? std::max(1, std::min(8, atoi(e))) : 0;
+  }();
   if (!on) return 1;
   const int tiles = ((M + 255) / 256) * ((N + 255) / 256);
   const int pairs = num_sms() / 2;
   const int kb = (K + kBK - 1) / kBK;
+  if (forced) return std::min(forced, std::max(1, kb / 4));
   if (tiles >= pairs) return 1;
   return std::max(1, std::min(std::min(pairs / tiles, kb / min_kbs), 8));
 }
