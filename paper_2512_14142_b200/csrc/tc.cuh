@@ -199,6 +199,30 @@ __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned l
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Sums of MT per-lane values over a warp, written to out[0..MT): recursive
+// halving -- at each step a lane keeps half of its values and adds its
+// partner's copy of them (MT/2 + MT/4 + ... shuffles, then a butterfly over
+// the remaining lane bits), 2*MT - 1 + log2(32 / MT) shuffles in all instead
+// of 5 * MT. MT: power of two <= 32. v is clobbered.
+template <int MT>
+__device__ __forceinline__ void warp_multi_sum(float* v, int lane, float* out) {
+  int base = 0;
+#pragma unroll
+  for (int w = MT, o = 16; w > 1; w >>= 1, o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < w / 2; ++i) {
+      const float send = up ? v[i] : v[i + w / 2];
+      const float keep = up ? v[i + w / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+    if (up) base += w / 2;
+  }
+#pragma unroll
+  for (int o = 16 / MT; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+  if ((lane & (32 / MT - 1)) == 0) out[base] = v[0];
+}
+
 // Finish one 128-feature tile: thread `row` holds v[t] (t < M) of feature
 // tile*128 + row. All 128 epilogue threads call this together. MT (<= BN):
 // compile-time bound of the token loops (MT = 1 for a batch of one keeps the
@@ -243,10 +267,11 @@ __device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* 
     }
     if (e.ssq_out) {
       const int q = row >> 5, lane = row & 31;
-#pragma unroll
-      for (int t = 0; t < MT; ++t) {
-        const float s = warp_sum(sq[t]);
-        if (lane == 0) red[q * BN + t] = s;
+      if constexpr (MT <= 32) {
+        warp_multi_sum<MT>(sq, lane, red + q * BN);
+      } else {
+        warp_multi_sum<32>(sq, lane, red + q * BN);
+        warp_multi_sum<32>(sq + 32, lane, red + q * BN + 32);
       }
       epi_bar();
       if (row < M) e.ssq_out[(long long)tile * M + row] = red[row] + red[BN + row] + red[2 * BN + row] + red[3 * BN + row];
