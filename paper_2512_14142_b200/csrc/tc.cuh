@@ -163,7 +163,8 @@ __device__ __forceinline__ void qkv_store(const Epi& e, bf16* C, int ldc, int t,
   if (slot < 0) return;
   const int kv = head < e.Hq + e.Hkv ? 0 : 1;
   const int h = head - e.Hq - kv * e.Hkv;
-  const int blk = slot / e.bt, off = slot % e.bt;
+  const int blk = e.bt == 16 ? slot >> 4 : slot / e.bt;   // 16-token pages: no integer division
+  const int off = e.bt == 16 ? slot & 15 : slot % e.bt;
   bf16* base = e.pool + (long long)blk * e.block_el + ((long long)(e.layer * 2 + kv) * e.Hkv + h) * e.bt * e.D;
   base[(long long)off * e.D + hrow] = f2bf(y);
 }
