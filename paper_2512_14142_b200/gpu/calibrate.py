@@ -88,9 +88,9 @@ def calibrate(dp, prefill_points=(128, 256, 512, 1024, 2048), decode_batches=(1,
     }
 
 
-def predictor_from_calibration(host, cal: dict):
-    """A host ServiceTimePredictor with the measured tables (API means keep the
+def predictor_from_calibration(ns, cal: dict):
+    """A reference ServiceTimePredictor with the measured tables (API means keep the
     reference defaults: API latency is the environment's, not the GPU's)."""
     cfg = dict(cal["predictor"])
-    cfg["api_latency_means"] = host.ServiceTimePredictor().to_config()["api_latency_means"]
-    return host.ServiceTimePredictor.from_config(cfg)
+    cfg["api_latency_means"] = ns.ServiceTimePredictor().to_config()["api_latency_means"]
+    return ns.ServiceTimePredictor.from_config(cfg)

@@ -1,8 +1,8 @@
 """KvDataPath: the device side of every KV transition and every batch.
 
-The host KV manager (``host.kvpolicy.KvCacheManager``) forwards the eight
-transitions of SURVEY.md Appendix C here; the GPU engine hands every
-admitted batch to :meth:`KvDataPath.launch_batch`.
+The reference's KV manager, subclassed in ``plugin.py`` (kvcache.py:152-292),
+forwards the eight transitions of SURVEY.md Appendix C here; the plugin's
+engine hands every admitted batch to :meth:`KvDataPath.launch_batch`.
 
 Streams
   compute  prefill + decode of batches, in admission order;
@@ -33,13 +33,15 @@ from typing import Optional
 import numpy as np
 import torch
 
-from ..host.errors import ProtocolError
-from ..host.trace import segment_token_ids
+from ..reference import load as _load_reference
+from ..tokens import segment_token_ids
 from . import lib as L
 from . import ops
 from .model import LlamaConfig, LlamaRunner, LlamaWeights
 
 BT = 16
+ProtocolError = _load_reference().ProtocolError   # the reference's own (errors.py:25)
+RESULTS_SOFT_LIMIT = 256
 
 
 class KvPool:
@@ -105,7 +107,7 @@ class KvDataPath:
                       "swap_out_bytes": 0, "swap_in_bytes": 0, "swap_outs": 0, "swap_ins": 0,
                       "discards": 0, "recompute_tokens": 0, "h2d_bytes": 0, "d2h_bytes": 0,
                       "kernel_launches": 0}
-        self.results: list = []     # (pinned hist copy, event, members) per batch for readback
+        self.results: list = []     # (event, pinned hist copy) per batch; see drain_results()
         self.use_graphs = True
         self._graphs: dict = {}
         self._graph_pool = None
@@ -233,12 +235,21 @@ class KvDataPath:
     def launch_batch(self, members) -> Optional[list]:
         """Transition 1 + the batch itself: (re)prefill, then the decode loop.
 
-        ``members`` are ``host.engine.AdmittedMember`` (pre-admission cache
+        ``members`` are ``plugin.AdmittedMember`` (pre-admission cache
         location). Returns per-member seconds when ``measure`` is set.
         """
         cfg = self.cfg
         dev = self.device
         B = len(members)
+        # reserve every member's blocks up front: a batch the pool cannot hold
+        # fails before any member's device state changes
+        grow = 0
+        for m in members:
+            rd = self.reqs.get(m.state.spec.id)
+            held = len(rd.blocks) if rd is not None else 0
+            grow += max(0, _blocks_for(m.state.context_after(m.segment_index)) - held)
+        if grow > self.pool.alloc.free:
+            raise ProtocolError(f"batch needs {grow} KV blocks, only {self.pool.alloc.free} free")
         plan = []
         pieces_meta = []   # per prefill member: list of device pieces or ("new", offset, n)
         new_ids_host = []
@@ -423,6 +434,8 @@ class KvDataPath:
             rb = torch.cuda.Event()
             rb.record(self.compute)
             self.results.append((rb, hist_host))
+            if len(self.results) > RESULTS_SOFT_LIMIT:   # nobody drains: keep only what is in flight
+                self.results = [(e, h) for e, h in self.results if not e.query()]
         # ---- host bookkeeping (no sync)
         for i, (m, p) in enumerate(zip(members, plan)):
             rd = p["rd"]
@@ -488,6 +501,22 @@ class KvDataPath:
         return g
 
     # ------------------------------------------------------------------ end of run
+
+    def reset(self) -> None:
+        """Abandon every request and return all blocks (a replay that was
+        stopped part-way, e.g. the bench's e2e window)."""
+        self.synchronize()
+        for rd in self.reqs.values():
+            if rd.blocks:
+                self.pool.alloc.give(rd.blocks)
+        self.reqs.clear()
+        self._fences.clear()
+        self.results = []
+
+    def drain_results(self) -> list:
+        """Hand over (and forget) every batch's (event, pinned tokens) readback."""
+        out, self.results = self.results, []
+        return out
 
     def synchronize(self) -> None:
         self.compute.synchronize()

@@ -13,7 +13,11 @@ import ctypes
 import os
 from pathlib import Path
 
-from ..host.errors import DeviceError
+
+
+class DeviceError(RuntimeError):
+    """The native CUDA library returned a non-zero status, or it / the
+    sm_100 device is missing (there is no CPU fallback)."""
 
 LIB_PATH = Path(os.environ.get("ASTRAEA_LIB", Path(__file__).resolve().parent.parent / "lib" / "libastraea_b200.so"))
 

@@ -15,7 +15,7 @@ from oracle import llama_ref  # noqa: E402
 from paper_2512_14142_b200.gpu.datapath import KvPool  # noqa: E402
 from paper_2512_14142_b200.gpu.model import PRESETS, LlamaWeights  # noqa: E402
 from paper_2512_14142_b200.gpu.tp import TpLlamaRunner, shard_config, shard_logical  # noqa: E402
-from paper_2512_14142_b200.host import segment_token_ids  # noqa: E402
+from paper_2512_14142_b200.tokens import segment_token_ids  # noqa: E402
 
 
 def run(rank, world, model="small"):

@@ -14,7 +14,8 @@ import torch.distributed as dist  # noqa: E402
 def shard_report(rank, world, n_per_rank):
     import argparse
     import bench
-    from paper_2512_14142_b200 import host
+    from paper_2512_14142_b200 import reference
+    host = reference.load()
     args = argparse.Namespace(qps=4.0, requests=n_per_rank, capacity=6000)
     shard, pred = bench.build_workload(args, rank, world)
     pol, mem, cfg = bench.make_run(host, shard, pred, args, 131072)

@@ -9,7 +9,7 @@ import pytest
 
 from paper_2512_14142_b200.gpu import lib as L
 from paper_2512_14142_b200.gpu.ops import BlockAllocator
-from paper_2512_14142_b200.host.errors import DeviceError
+from paper_2512_14142_b200.gpu.lib import DeviceError
 
 HEADER = Path(__file__).resolve().parent.parent / "include" / "astraea_b200.h"
 

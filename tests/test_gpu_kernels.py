@@ -67,7 +67,7 @@ def test_swap_out_matches_oracle_and_round_trips_bit_exact(mode, Lyr, Hkv, D, n_
 def test_swap_rejects_bad_arguments():
     pool, geo = make_pool(8, 2, 2, 64)
     slot = torch.zeros(100 * 2 * 2 * 2 * 64 * 2, dtype=torch.uint8, pin_memory=True)
-    from paper_2512_14142_b200.host.errors import DeviceError
+    from paper_2512_14142_b200.gpu.lib import DeviceError
     with pytest.raises(DeviceError):
         ops.swap_out(geo, pool, [0, 1], 100, slot)          # 100 tokens need 7 blocks
     with pytest.raises(DeviceError):

@@ -16,9 +16,13 @@ pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="
 from paper_2512_14142_b200.gpu import ops  # noqa: E402
 from paper_2512_14142_b200.gpu.datapath import KvPool  # noqa: E402
 from paper_2512_14142_b200.gpu.model import PRESETS, LlamaRunner, LlamaWeights  # noqa: E402
-from paper_2512_14142_b200.host import (CacheLocation, RequestSpec, RequestState,  # noqa: E402
-                                        SegmentSpec, segment_token_ids)
-from paper_2512_14142_b200.host.engine import AdmittedMember  # noqa: E402
+from paper_2512_14142_b200 import reference  # noqa: E402
+from paper_2512_14142_b200.plugin import AdmittedMember  # noqa: E402
+from paper_2512_14142_b200.tokens import segment_token_ids  # noqa: E402
+
+_ref = reference.load()
+CacheLocation, RequestState = _ref.scheduler.CacheLocation, _ref.RequestState
+RequestSpec, SegmentSpec = _ref.RequestSpec, _ref.SegmentSpec
 
 DEV = "cuda"
 

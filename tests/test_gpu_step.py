@@ -13,7 +13,7 @@ pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="
 
 from paper_2512_14142_b200.gpu.datapath import KvPool  # noqa: E402
 from paper_2512_14142_b200.gpu.model import PRESETS, LlamaConfig, LlamaRunner, LlamaWeights  # noqa: E402
-from paper_2512_14142_b200.host import segment_token_ids  # noqa: E402
+from paper_2512_14142_b200.tokens import segment_token_ids  # noqa: E402
 
 DEV = "cuda"
 # head_dim 128 with 4 q heads per kv head (the Llama-3-8B attention shape) at

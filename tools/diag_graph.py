@@ -11,7 +11,8 @@ import torch  # noqa: E402
 
 import scenarios  # noqa: E402
 from gpu_util import datapath_for  # noqa: E402
-from paper_2512_14142_b200 import host  # noqa: E402
+from paper_2512_14142_b200 import reference  # noqa: E402
+host = reference.load()   # the unmodified reference package
 from paper_2512_14142_b200.gpu.datapath import KvDataPath  # noqa: E402
 from paper_2512_14142_b200.gpu.engine import GpuEngine  # noqa: E402
 

@@ -10,9 +10,11 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import torch
 
 import bench
-from paper_2512_14142_b200 import host
+from paper_2512_14142_b200 import reference
+host = reference.load()   # the unmodified reference package
 from paper_2512_14142_b200.gpu import lib as L
 from paper_2512_14142_b200.gpu.datapath import KvDataPath
+from paper_2512_14142_b200 import plugin
 from paper_2512_14142_b200.gpu.engine import GpuEngine
 from paper_2512_14142_b200.gpu.model import PRESETS
 
@@ -27,6 +29,6 @@ for i in range(3):
     rep = GpuEngine(shard, pol, pred, mem, scfg, dp, clock="measured").run()
     agg = rep.aggregates()
     print(json.dumps({"run": i, "avg_jct": agg["avg_jct"], "p99_jct": agg["p99_jct"],
-                      "req_per_s": rep.requests_per_second(),
+                      "req_per_s": plugin.requests_per_second(rep),
                       "device": {k: rep.device[k] for k in ("batches", "prefill_tokens", "decode_steps", "swap_outs",
                                                             "swap_ins", "discards", "recompute_tokens")}}), flush=True)

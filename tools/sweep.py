@@ -1,6 +1,6 @@
 """Memory-pressure (C3) and request-rate (C4) sweeps of the B200 data path.
 
-For each cell: the reference scheduler (host mirror, decisions byte-identical
+For each cell: the reference scheduler (the unmodified reference, decisions byte-identical
 to the reference -- asserted against a host-only run) drives the Llama-3-8B
 data path; the clock advances by B200-measured batch and swap durations
 (``clock="measured"``; API waits stay virtual). Reported per cell: avg / p99
@@ -22,8 +22,10 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
 import scenarios  # noqa: E402
-from paper_2512_14142_b200 import host  # noqa: E402
+from paper_2512_14142_b200 import reference  # noqa: E402
+host = reference.load()   # the unmodified reference package
 from paper_2512_14142_b200.gpu.datapath import KvDataPath  # noqa: E402
+from paper_2512_14142_b200 import plugin  # noqa: E402
 from paper_2512_14142_b200.gpu.engine import GpuEngine  # noqa: E402
 from paper_2512_14142_b200.gpu.model import PRESETS  # noqa: E402
 
@@ -51,7 +53,7 @@ def cell(wl, capacity, tables, dp):
                 host.MemoryModel(capacity_tokens=capacity, bytes_per_token=float(cfg.kv_bytes_per_token),
                                  swap_bandwidth_tokens_per_s=bw),
                 host.SimConfig(cost_model="parallel-max", cache_mode="adaptive"))
-    ref = host.Engine(wl, *parts()).run()
+    ref = host.run(wl, *parts())
     t0 = time.time()
     dev0 = dict(dp.stats)
     model = GpuEngine(wl, *parts(), dp, clock="model").run()
@@ -62,9 +64,9 @@ def cell(wl, capacity, tables, dp):
     return {"capacity_tokens": capacity, "cost_tables": tables, "requests": len(wl),
             "kv_actions": dict(acts),
             "measured_clock": {"avg_jct_s": agg_m["avg_jct"], "p99_jct_s": agg_m["p99_jct"],
-                               "req_per_s": measured.requests_per_second()},
+                               "req_per_s": plugin.requests_per_second(measured)},
             "model_clock": {"avg_jct_s": agg_s["avg_jct"], "p99_jct_s": agg_s["p99_jct"],
-                            "req_per_s": model.requests_per_second()},
+                            "req_per_s": plugin.requests_per_second(model)},
             # device work of the measured-clock run (same plans as the model-clock run)
             "device": {k: (measured.device[k] - dev0[k]) // 2 for k in
                        ("batches", "prefill_tokens", "decode_steps", "swap_outs", "swap_ins", "discards",
