@@ -8,12 +8,14 @@ What is pinned and how:
 
 * Scheduling order and KV-policy decisions: pinned to the reference itself
   (pkg/src/agentsched, run unmodified in the build container by
-  tests/golden/make_golden.py; 76 scenarios, SHA-256 of RunReport.to_json).
+  tests/golden/make_golden.py; 79 scenarios, SHA-256 of RunReport.to_json).
 * KV block bytes (swap gather/scatter, table build, append slots): integer /
   byte work restated in numpy here (``kvpool_ref``); exact equality required.
 * Attention, GEMM, RMSNorm, RoPE, SiLU, the Llama forward: fp32 torch on CPU
-  (``attention_ref``, ``llama_ref``). **Parity unpinned**: the reference has
-  no model, no tensors and no dependency implementing one (SURVEY.md
-  section 0, pyproject dependencies = []), so these restate the standard
-  Llama-3 architecture; the tolerance is the north star's 1e-2 relative.
+  (``attention_ref``, ``llama_ref``). The reference has no model (SURVEY.md
+  section 0), so these restate Llama-3; the restatement is **pinned to
+  Hugging Face transformers' ``LlamaForCausalLM``** (5.5.0, in the image) on
+  identical weights -- logits, greedy continuation, the paged decode over
+  HF's cached K/V and the TP restatement agree to fp32 rounding
+  (tests/test_oracle_pin.py). Device tolerance: north star's 1e-2 relative.
 """

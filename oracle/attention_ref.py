@@ -1,6 +1,7 @@
 """fp32 CPU restatement of paged decode / prefill attention (test oracle).
 
-Parity unpinned (no reference implementation exists; see oracle/__init__).
+Pinned to transformers' Llama attention through its cached K/V
+(tests/test_oracle_pin.py); the reference has no model (oracle/__init__).
 Follows the standard scaled-dot-product attention with GQA and causal
 masking on absolute positions, reading K/V through the same block table the
 CUDA kernels read.

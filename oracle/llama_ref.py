@@ -1,6 +1,7 @@
 """fp32 CPU restatement of the Llama-3 decoder the data path runs (test oracle).
 
-Parity unpinned (see oracle/__init__): the reference has no model. This is
+Pinned to transformers' LlamaForCausalLM (tests/test_oracle_pin.py); the
+reference itself has no model (see oracle/__init__). This is
 the textbook Llama-3 block -- RMSNorm, RoPE (NeoX half split, theta
 500000), grouped-query attention, SwiGLU MLP -- over a contiguous causal
 sequence, i.e. *without* paging, so the device's paged KV, block tables,
