@@ -133,12 +133,15 @@ def engine_classes(ns=None):
             pool = getattr(datapath, "pool", None)
             if pool is not None:
                 # token-exact admission must always be block-feasible: every
-                # resident request may round up to one partial block
-                need = math.ceil(memory.capacity_tokens / 16) + len(self.workload)
+                # resident request may round up to one partial block. Resident
+                # tokens never exceed the capacity nor the whole trace's context.
+                trace_tokens = sum(s.n_in + s.n_gen for r in self.workload for s in r.segments)
+                peak = min(memory.capacity_tokens, trace_tokens)
+                need = math.ceil(peak / 16) + len(self.workload)
                 if pool.num_blocks < need:
-                    raise ns.ConfigError(f"KV pool of {pool.num_blocks} blocks cannot back capacity "
-                                         f"{memory.capacity_tokens} tokens with {len(self.workload)} requests "
-                                         f"(needs {need})")
+                    raise ns.ConfigError(f"KV pool of {pool.num_blocks} blocks cannot back "
+                                         f"{peak} resident tokens (capacity {memory.capacity_tokens}) with "
+                                         f"{len(self.workload)} requests (needs {need})")
             self.manager = GpuKvCacheManager(memory, predictor, mode=config.cache_mode)
             self.manager.device = datapath
             self.manager.engine = self

@@ -68,3 +68,25 @@ def test_no_restated_scheduler_in_the_package():
         for sym in ("def hrrn_score", "def estimate_waste", "def _pack_greedy", "def execute_batch",
                     "class StatefulMlfqPolicy", "class MemoryModel"):
             assert sym not in text, (src, sym)
+
+
+def test_pool_size_check_bounds_by_capacity_and_trace():
+    """The block-feasibility check (GpuEngine.__init__) needs ceil(peak/16)
+    + one partial block per request, peak = min(capacity, the whole trace's
+    context): fig2 (capacity 1e6, 12 tokens of context) fits 512 blocks, as
+    __graft_entry__.smoke() runs it; a pool short of a block is refused."""
+    import math
+    import types
+    wl, pol, pred, mem, cfg = scenarios.build(ref, "fig2/fcfs")
+    rec = Recorder()
+    GpuEngine = plugin.engine_classes(ref)[1]
+    rec.pool = types.SimpleNamespace(num_blocks=512)
+    GpuEngine(wl, pol, pred, mem, cfg, rec)   # accepted
+    wl, pol, pred, mem, cfg = scenarios.build(ref, "c1b200/6000")
+    peak = min(mem.capacity_tokens, sum(s.n_in + s.n_gen for r in wl for s in r.segments))
+    rec.pool = types.SimpleNamespace(num_blocks=math.ceil(peak / 16) + len(wl) - 1)
+    with pytest.raises(ref.ConfigError):
+        GpuEngine(wl, pol, pred, mem, cfg, rec)
+    rec.pool.num_blocks += 1
+    wl, pol, pred, mem, cfg = scenarios.build(ref, "c1b200/6000")
+    GpuEngine(wl, pol, pred, mem, cfg, rec)
