@@ -28,22 +28,26 @@ def rmsnorm(x, w, eps):
 
 def rope(x, positions, theta):
     D = x.shape[-1]
-    inv = 1.0 / (theta ** (torch.arange(0, D, 2, dtype=torch.float32) / D))
+    inv = 1.0 / (theta ** (torch.arange(0, D, 2, dtype=torch.float32, device=x.device) / D))
     ang = positions.float().unsqueeze(1) * inv.unsqueeze(0)
     cos, sin = ang.cos().unsqueeze(1), ang.sin().unsqueeze(1)
     x1, x2 = x[..., : D // 2], x[..., D // 2:]
     return torch.cat([x1 * cos - x2 * sin, x2 * cos + x1 * sin], dim=-1)
 
 
-def forward(w, cfg, ids, bf16_points=True):
-    """Logits [T, vocab] (fp32) for one sequence of token ids starting at position 0."""
+def forward(w, cfg, ids, bf16_points=True, last_only=False):
+    """Logits [T, vocab] (fp32) for one sequence of token ids starting at position 0
+    (``last_only``: [1, vocab], the last position's). Runs on the device the
+    weights ``w`` live on (CPU for the unit tests; the 8B-shape GPU tests keep
+    the same fp32 arithmetic on the GPU with TF32 off)."""
     T = len(ids)
     Hq, Hkv, D = cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim
     G = Hq // Hkv
     r = lambda t: _r(t, bf16_points)  # noqa: E731
-    pos = torch.arange(T)
-    x = w["embed"][torch.as_tensor(ids, dtype=torch.long)].float()
-    mask = torch.triu(torch.ones(T, T, dtype=torch.bool), 1)
+    dev = w["embed"].device
+    pos = torch.arange(T, device=dev)
+    x = w["embed"][torch.as_tensor(ids, dtype=torch.long, device=dev)].float()
+    mask = torch.triu(torch.ones(T, T, dtype=torch.bool, device=dev), 1)
     for lw in w["layers"]:
         h = rmsnorm(x, lw["attn_norm"].float(), cfg.eps)
         qkv = r(h @ lw["wqkv"].float().T)
@@ -63,6 +67,8 @@ def forward(w, cfg, ids, bf16_points=True):
         g, u = gu[:, : cfg.ffn], gu[:, cfg.ffn:]
         m = r(r(torch.nn.functional.silu(g)) * u)
         x = r(m @ lw["wdown"].float().T + x)
+    if last_only:
+        x = x[-1:]
     h = rmsnorm(x, w["final_norm"].float(), cfg.eps)
     return h @ w["lm_head"].float().T
 

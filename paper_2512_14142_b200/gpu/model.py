@@ -170,24 +170,25 @@ class LlamaWeights:
         self.lm_head = dv(fold(wd["lm_head"], wd["final_norm"]))
         return self
 
-    def to_cpu_dict(self) -> dict:
+    def to_cpu_dict(self, device="cpu") -> dict:
         """Logical weights: un-interleaved gate/up, norms separate (the
-        stored projections are W diag(norm); with unit norms that is W)."""
+        stored projections are W diag(norm); with unit norms that is W).
+        ``device``: where the copies live (the oracle runs there)."""
 
         def unfold(weight, norm):
-            return (weight.float() / norm.float()[None, :]).to(torch.bfloat16).cpu()
+            return (weight.float() / norm.float()[None, :]).to(torch.bfloat16).to(device)
 
         layers = []
         for lw in self.layers:
             layers.append({
-                "attn_norm": lw["attn_norm"].cpu(),
-                "mlp_norm": lw["mlp_norm"].cpu(),
+                "attn_norm": lw["attn_norm"].to(device),
+                "mlp_norm": lw["mlp_norm"].to(device),
                 "wqkv": unfold(lw["wqkv"], lw["attn_norm"]),
-                "wo": lw["wo"].cpu(),
+                "wo": lw["wo"].to(device),
                 "wgu": unfold(deinterleave_gate_up(lw["wgu"], self.cfg.ffn), lw["mlp_norm"]),
-                "wdown": lw["wdown"].cpu(),
+                "wdown": lw["wdown"].to(device),
             })
-        return {"embed": self.embed.cpu(), "layers": layers, "final_norm": self.final_norm.cpu(),
+        return {"embed": self.embed.to(device), "layers": layers, "final_norm": self.final_norm.to(device),
                 "lm_head": unfold(self.lm_head, self.final_norm)}
 
 
@@ -334,8 +335,6 @@ class LlamaRunner:
             return self._decode_unchained(tokens, positions, slots, table, ctx, stream, want_logits, keys_out)
         if self.use_step_kernel and self._step_supported():
             return self._decode_step_kernel(tokens, positions, slots, table, ctx, stream, keys_out, want_logits)
-        if want_logits:
-            return self._decode_unchained(tokens, positions, slots, table, ctx, stream, want_logits, keys_out)
         if not self.use_chain:
             return self._decode_unchained(tokens, positions, slots, table, ctx, stream, want_logits, keys_out)
         cfg, w, pool = self.cfg, self.w, self.pool
@@ -352,6 +351,9 @@ class LlamaRunner:
         ssq_mid = torch.empty(self.parts, B, dtype=torch.float32, device=dev)
         ssq = torch.empty(self.parts, B, dtype=torch.float32, device=dev)
         keys = keys_out if keys_out is not None else torch.zeros(B, dtype=torch.int64, device=dev)
+        # the last layer's chain ends with lm_head + argmax; it also writes the
+        # logits when asked (same epilogue, C non-null)
+        logits = torch.empty(B, cfg.vocab, dtype=torch.bfloat16, device=dev) if want_logits else None
         cs = ops.rope_table(positions, cfg.head_dim, cfg.rope_theta, stream=stream)
 
         def qkv(li, ssq_in):
@@ -381,12 +383,13 @@ class LlamaRunner:
                 if li + 1 < cfg.num_layers:
                     phases.append(qkv(li + 1, ssq))
                 else:
-                    phases.append(dict(a=x, w=w.lm_head, out=None, kind=L.EPI_ARGMAX, ssq_in=ssq, rms_dim=d,
+                    phases.append(dict(a=x, w=w.lm_head, out=logits, kind=L.EPI_ARGMAX, ssq_in=ssq, rms_dim=d,
                                        rms_eps=eps, argmax_keys=keys))
             ops.gemm_chain(phases, ws, stream=stream, attn=attns or None)
         if keys_out is not None:
-            return keys_out
-        return ops.keys_to_ids(keys)
+            return (keys_out, logits) if want_logits else keys_out
+        ids = ops.keys_to_ids(keys)
+        return (ids, logits) if want_logits else ids
 
     def _attn_fusable(self) -> bool:
         cfg = self.cfg

@@ -1,0 +1,125 @@
+"""Logits parity at the Llama-3-8B layer shape the bench times (d 4096, 32 q
+heads / 8 kv heads of 128, ffn 14336, vocab 128256; two decoder layers so
+the fp32 oracle stays fast): the 512-token varlen prefill (CTA-pair tcgen05
+GEMMs, paged prefill attention) and the fused decode step (one launch per
+layer: paged attention -> O -> gate/up -> down -> next QKV; the last layer
+ends in lm_head + argmax and writes the logits) at B in {1, 8, 16}, eager
+and replayed from a CUDA graph, against oracle/llama_ref.py (pinned to
+transformers' LlamaForCausalLM by tests/test_oracle_pin.py).
+
+The oracle runs on the GPU in fp32 with TF32 off -- the same arithmetic as on
+the CPU, only faster at this shape. Bar: relative L2 <= 1e-2 (north_star's
+bf16 logits tolerance)."""
+
+import pytest
+import torch
+
+from conftest import cuda_available
+from oracle import llama_ref
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="needs a B200")]
+
+from paper_2512_14142_b200.gpu.datapath import KvPool  # noqa: E402
+from paper_2512_14142_b200.gpu.model import LlamaConfig, LlamaRunner, LlamaWeights  # noqa: E402
+from paper_2512_14142_b200.tokens import segment_token_ids  # noqa: E402
+
+DEV = "cuda"
+TOL = 1e-2
+CFG = LlamaConfig("llama3-8b-2l", 2, 4096, 32, 8, 128, 14336, 128256)
+
+
+def rel(a, b):
+    a, b = a.float(), b.float()
+    return float((a - b).norm() / b.norm())
+
+
+@pytest.fixture(scope="module")
+def model():
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    w = LlamaWeights(CFG, seed=11)
+    logical = w.to_cpu_dict(device=DEV)   # the oracle's (textbook) weights, on the GPU
+    return w, logical
+
+
+def d(v):
+    return torch.tensor(v, dtype=torch.int32, device=DEV)
+
+
+def oracle_last(logical, ids):
+    with torch.no_grad():
+        return llama_ref.forward(logical, CFG, ids, last_only=True)[0]
+
+
+def prefill(runner, seqs, tables):
+    """One varlen prefill of every sequence (positions 0..T-1)."""
+    ids, pos, slots, cu, last = [], [], [], [0], []
+    for s, blocks in zip(seqs, tables):
+        T = len(s)
+        ids += s
+        pos += list(range(T))
+        slots += [blocks[p // 16] * 16 + p % 16 for p in range(T)]
+        cu.append(cu[-1] + T)
+        last.append(cu[-1] - 1)
+    width = max(len(t) for t in tables)
+    table = d([t + [-1] * (width - len(t)) for t in tables])
+    return runner.prefill(d(ids), d(pos), d(slots), d(cu), table, d([len(s) for s in seqs]),
+                          torch.tensor(last, device=DEV), max(len(s) for s in seqs), want_logits=True)
+
+
+def test_8b_shape_prefill_512_logits(model):
+    w, logical = model
+    pool = KvPool(CFG, 64)
+    runner = LlamaRunner(w, pool)
+    ids = segment_token_ids("p512", 1, 512, CFG.vocab)
+    tok, logits = prefill(runner, [ids], [list(range(3, 35))])
+    ref = oracle_last(logical, ids)
+    assert rel(logits[0], ref) < TOL
+
+
+@pytest.mark.parametrize("B", [1, 8, 16])
+def test_8b_shape_fused_decode_logits(model, B):
+    """Two fused decode steps after a varlen prefill of B ragged sequences
+    (contexts 40..700, scattered blocks): step 1 eager, step 2 replayed from
+    a CUDA graph (the data path's decode loop); every row's logits vs the
+    oracle on that row's whole sequence."""
+    w, logical = model
+    per = 46   # blocks per row: room for 700 + 2 tokens
+    pool = KvPool(CFG, B * per + 8)
+    runner = LlamaRunner(w, pool)
+    assert runner.use_chain and runner.fuse_attention and runner._attn_fusable()
+    lens = [40 + (660 * b) // max(1, B - 1) for b in range(B)]
+    seqs = [segment_token_ids(f"r{b}", 1, lens[b], CFG.vocab) for b in range(B)]
+    perm = torch.randperm(B * per, generator=torch.Generator().manual_seed(B)).tolist()
+    tables = [perm[b * per:(b + 1) * per] for b in range(B)]
+    tok, _ = prefill(runner, seqs, tables)
+    nxt = tok.tolist()
+    table = d(tables)
+    graph = None
+    for step in range(2):
+        pos = [len(s) for s in seqs]
+        for b in range(B):
+            seqs[b] = seqs[b] + [int(nxt[b])]
+        args = dict(tokens=d([s[-1] for s in seqs]), positions=d(pos),
+                    slots=d([tables[b][p // 16] * 16 + p % 16 for b, p in enumerate(pos)]), table=table,
+                    ctx=d([p + 1 for p in pos]))
+        if step == 0:
+            out, logits = runner.decode(**args, want_logits=True)
+        else:
+            static = {k: v.clone() for k, v in args.items()}
+            runner.decode(**static, want_logits=True)   # warm-up (rewrites the same K/V rows)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                out, logits = runner.decode(**static, want_logits=True)
+            graph.replay()
+        torch.cuda.synchronize()
+        for b in range(B):
+            ref = oracle_last(logical, seqs[b])
+            e = rel(logits[b], ref)
+            assert e < TOL, (step, b, lens[b], e)
+        # greedy tokens: the sampled token holds the row's largest logit
+        lf = logits.float()
+        assert torch.equal(lf.gather(1, out.long().view(-1, 1)).view(-1), lf.max(-1).values), step
+        nxt = out.tolist()
+    assert graph is not None

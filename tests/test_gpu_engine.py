@@ -65,3 +65,29 @@ def test_graph_and_eager_decode_paths_agree():
         GpuEngine(wl, pol, pred, mem, cfg, dp).run()
         toks[graphs] = [h.cpu().tolist() for _, h in dp.drain_results()]
     assert toks[True] == toks[False]
+
+
+@pytest.fixture(scope="module")
+def w8b():
+    from paper_2512_14142_b200.gpu.model import PRESETS, LlamaWeights
+    return LlamaWeights(PRESETS["llama3-8b"], seed=0)
+
+
+@pytest.mark.parametrize("name", ["c2/12000", "c2/40000"])
+def test_8b_engine_c2_report_matches_reference(name, golden, w8b):
+    """The bench's model (Llama-3-8B shape) executing every plan of the C2
+    trace (64 requests, the reference's default tables, 131,072 B/token):
+    the report is byte-identical to the reference's golden, the device saw
+    the golden's swap and discard decisions, and every block came back."""
+    from paper_2512_14142_b200.gpu.model import PRESETS
+    wl, pol, pred, mem, cfg = scenarios.build(host, name)
+    dp = datapath_for(mem.capacity_tokens, model="llama3-8b", weights=w8b)
+    assert dp.pool.bytes_per_token == 131072
+    rep = GpuEngine(wl, pol, pred, mem, cfg, dp, clock="model").run()
+    assert hashlib.sha256(rep.to_json().encode()).hexdigest() == golden[name]["sha256"]
+    dev = rep.device
+    assert dev["free_blocks"] == dev["num_blocks"] and dev["decode_steps"] > 1000
+    decisions = golden[name]["kv_decisions"]
+    assert dev["swap_outs"] == decisions.get("swap:estimated", 0)
+    assert dev["discards"] == decisions.get("discard:estimated", 0) + decisions.get("discard:deadlock-evicted", 0)
+    assert PRESETS["llama3-8b"].kv_bytes_per_token == 131072
