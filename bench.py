@@ -70,7 +70,9 @@ def parse(argv=None):
     ap.add_argument("--requests", type=int, default=64, help="requests per rank (C2: 64)")
     ap.add_argument("--qps", type=float, default=2.0, help="arrival rate per rank")
     ap.add_argument("--capacity", type=int, default=12000, help="KV capacity (tokens) per GPU")
-    ap.add_argument("--swap-mode", choices=("kernel", "dma"), default="kernel")
+    ap.add_argument("--swap-mode", choices=("kernel", "dma", "staged"), default="staged",
+                    help="K1/K2 path (tools/swap_load.py: staged keeps the host link at ~54 GB/s and slows a "
+                         "concurrent decode by ~4%%; the zero-copy SM kernel slows it 2x)")
     ap.add_argument("--cost-tables", choices=("calibrated", "b200-like", "reference"), default="calibrated",
                     help="scheduler cost tables: measured on the B200 (profiles/r1_b200_cost_tables.json), "
                          "the survey's B200-like guess, or the reference defaults")
@@ -390,7 +392,7 @@ def swap_under_load(dp, cfg, tokens, batch=4, steps=40, swaps=8):
     alone_dec = a.elapsed_time(b) / steps
     res["decode_step_ms_alone"] = alone_dec
     moved = 2 * swaps * tokens * dp.pool.bytes_per_token
-    for name, mode in (("kernel", L.SWAP_KERNEL), ("dma", L.SWAP_DMA)):
+    for name, mode in (("kernel", L.SWAP_KERNEL), ("dma", L.SWAP_DMA), ("staged", L.SWAP_STAGED)):
         swap_loop(mode)
         torch.cuda.synchronize()
         a, b = swap_loop(mode)
@@ -570,7 +572,8 @@ def main():
     s = window_start(n_b, args.steps, args.warmup)
     win = summarize(batches, s, args.steps)
     blocks = max(math.ceil(args.capacity / 16) + 2 * len(shard) + 64, 32 * 72)   # sweep room: B 32 x 1.1k ctx
-    dp = KvDataPath(cfg, num_blocks=blocks, swap_mode=L.SWAP_KERNEL if args.swap_mode == "kernel" else L.SWAP_DMA)
+    dp = KvDataPath(cfg, num_blocks=blocks, swap_mode={"kernel": L.SWAP_KERNEL, "dma": L.SWAP_DMA,
+                                                             "staged": L.SWAP_STAGED}[args.swap_mode])
     Engine = bench_engine()
 
     def replay(hook=None, clock="model"):
@@ -794,7 +797,7 @@ def swap_gbs(dp, cfg, tokens):
     ids = list(range(nb))
     slot = torch.empty(tokens * dp.pool.bytes_per_token, dtype=torch.uint8, pin_memory=True)
     res = {"tokens": tokens, "bytes": tokens * dp.pool.bytes_per_token}
-    for name, mode in (("kernel", L.SWAP_KERNEL), ("dma", L.SWAP_DMA)):
+    for name, mode in (("kernel", L.SWAP_KERNEL), ("dma", L.SWAP_DMA), ("staged", L.SWAP_STAGED)):
         for direction in ("out", "in"):
             fn = ops.swap_out if direction == "out" else ops.swap_in
             fn(dp.pool.geo, dp.pool.data, ids, tokens, slot, mode)
@@ -817,8 +820,8 @@ def swap_gbs(dp, cfg, tokens):
         e1.record()
         e1.synchronize()
         res[f"memcpy_{direction}_gbs"] = res["bytes"] * 5 / (e0.elapsed_time(e1) / 1000.0) / 1e9
-    best_out = max(res["kernel_out_gbs"], res["dma_out_gbs"])
-    best_in = max(res["kernel_in_gbs"], res["dma_in_gbs"])
+    best_out = max(res["kernel_out_gbs"], res["dma_out_gbs"], res["staged_out_gbs"])
+    best_in = max(res["kernel_in_gbs"], res["dma_in_gbs"], res["staged_in_gbs"])
     res["frac_out_vs_memcpy"] = best_out / res["memcpy_d2h_gbs"]
     res["frac_in_vs_memcpy"] = best_in / res["memcpy_h2d_gbs"]
     return res

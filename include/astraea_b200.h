@@ -91,9 +91,13 @@ ASTRAEA_API int32_t astraea_alloc_free_count(const astraea_block_allocator* a);
  * n_tokens tokens are moved (the last block's padding is not).
  * mode 0: SM gather/scatter kernel writing/reading the pinned slot through
  *         its mapped device address (zero-copy over the host link);
- * mode 1: copy engines, one strided 2-D DMA per block.
+ * mode 1: copy engines, one strided 2-D DMA per block;
+ * mode 2: staged -- the SM kernel gathers (scatters) the token-compact slot
+ *         image in a stream-ordered device buffer (HBM to HBM, tens of us)
+ *         and ONE contiguous copy-engine transfer crosses the host link, so
+ *         the SMs are busy only briefly beside a running decode.
  * host slot must be pinned (cudaHostAlloc / cudaHostRegister). */
-enum { ASTRAEA_SWAP_KERNEL = 0, ASTRAEA_SWAP_DMA = 1 };
+enum { ASTRAEA_SWAP_KERNEL = 0, ASTRAEA_SWAP_DMA = 1, ASTRAEA_SWAP_STAGED = 2 };
 ASTRAEA_API int astraea_kv_swap_out(const astraea_kv_geometry* g, const void* pool_dev,
                         const int32_t* block_ids_host, int32_t n_blocks, int32_t n_tokens,
                         void* slot_host, int mode, void* stream);

@@ -121,8 +121,12 @@ struct SwapArgs {
   int ids[kSwapMaxIds];
 };
 
+constexpr int kSwapCtas = 32;   // default grid of the SM swap path (tools/swap_load.py sweep)
+
+constexpr int kSwapThreads = 128;
+
 template <bool kOut>
-__global__ void __launch_bounds__(256) swap_kernel(const __grid_constant__ SwapArgs a) {
+__global__ void __launch_bounds__(kSwapThreads) swap_kernel(const __grid_constant__ SwapArgs a) {
   const int lane_id = threadIdx.x & 31;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -193,7 +197,7 @@ static int swap_impl(bool out, const astraea_kv_geometry* g, const void* pool, v
     }
     return ASTRAEA_OK;
   }
-  if (mode != ASTRAEA_SWAP_KERNEL) return ASTRAEA_EINVAL;
+  if (mode != ASTRAEA_SWAP_KERNEL && mode != ASTRAEA_SWAP_STAGED) return ASTRAEA_EINVAL;
   {
     // The SM path dereferences the slot over the host link: it must be pinned.
     cudaPointerAttributes attr;
@@ -203,8 +207,47 @@ static int swap_impl(bool out, const astraea_kv_geometry* g, const void* pool, v
       return ASTRAEA_EINVAL;
     }
   }
-  char* slot_dev = (char*)mapped(out ? slot_mut : slot);
-  const int grid = num_sms() * 2;
+  // Co-residence with the persistent decode kernel (1 CTA/SM, ~200 KB of
+  // shared memory): a swap CTA must not pin its SM to a small-shared-memory
+  // carveout (the decode CTA could then not start there until the swap CTA
+  // exits), and its registers must fit beside the decode CTA's.
+  static const bool carveout = [] {
+    cudaFuncSetAttribute(swap_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(swap_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    cudaGetLastError();
+    return true;
+  }();
+  (void)carveout;
+  const size_t slot_bytes = (size_t)n_tokens * row_bytes * lanes;
+  char* slot_dev = nullptr;
+  if (mode == ASTRAEA_SWAP_STAGED) {
+    // stream-ordered staging image of the slot; the device pool keeps freed
+    // memory cached (no release threshold), so steady-state swaps allocate nothing
+    static const bool pool_cfg = [] {
+      int dev = 0;
+      cudaMemPool_t mp;
+      if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      cudaGetLastError();
+      return true;
+    }();
+    (void)pool_cfg;
+    ASTRAEA_TRY(cudaMallocAsync((void**)&slot_dev, slot_bytes, st));
+    if (!out) ASTRAEA_TRY(cudaMemcpyAsync(slot_dev, slot, slot_bytes, cudaMemcpyHostToDevice, st));
+  } else {
+    slot_dev = (char*)mapped(out ? slot_mut : slot);
+  }
+  // A few CTAs keep the host link full (a warp moves up to 4 KiB per
+  // round trip); more only steal issue slots and memory-pipe share from the
+  // persistent decode kernel running beside the swap. ASTRAEA_SWAP_CTAS
+  // overrides (read per call, for the load sweeps).
+  const char* env = getenv("ASTRAEA_SWAP_CTAS");
+  const int grid = mode == ASTRAEA_SWAP_STAGED ? 2 * num_sms()   // HBM to HBM: a short full-width burst
+                                               : std::max(1, std::min(env ? atoi(env) : kSwapCtas, 4 * num_sms()));
   for (int32_t first = 0; first < n_blocks; first += kSwapMaxIds) {
     SwapArgs a;
     const int nb = std::min<int32_t>(kSwapMaxIds, n_blocks - first);
@@ -220,13 +263,17 @@ static int swap_impl(bool out, const astraea_kv_geometry* g, const void* pool, v
     if (out) {
       a.src = (const char*)pool;
       a.dst = slot_dev;
-      swap_kernel<true><<<grid, 256, 0, st>>>(a);
+      swap_kernel<true><<<grid, kSwapThreads, 0, st>>>(a);
     } else {
       a.src = slot_dev;
       a.dst = (char*)pool_mut;
-      swap_kernel<false><<<grid, 256, 0, st>>>(a);
+      swap_kernel<false><<<grid, kSwapThreads, 0, st>>>(a);
     }
     ASTRAEA_CHECK_LAUNCH();
+  }
+  if (mode == ASTRAEA_SWAP_STAGED) {
+    if (out) ASTRAEA_TRY(cudaMemcpyAsync(slot_mut, slot_dev, slot_bytes, cudaMemcpyDeviceToHost, st));
+    ASTRAEA_TRY(cudaFreeAsync(slot_dev, st));
   }
   return ASTRAEA_OK;
 }

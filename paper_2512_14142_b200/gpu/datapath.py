@@ -87,7 +87,7 @@ def _loc(location) -> str:
 
 class KvDataPath:
     def __init__(self, cfg: LlamaConfig, weights: Optional[LlamaWeights] = None, num_blocks: int = 4096,
-                 device="cuda", swap_mode: int = L.SWAP_KERNEL, seed: int = 0, measure: bool = False,
+                 device="cuda", swap_mode: int = L.SWAP_STAGED, seed: int = 0, measure: bool = False,
                  token_seed: int = 0):
         L.require_cuda()
         self.cfg = cfg
@@ -178,7 +178,7 @@ class KvDataPath:
         rd.slot, rd.slot_tokens, rd.swap_ev = slot, n, (s0, s1)
         self.stats["swap_out_bytes"] += n * self.pool.bytes_per_token
         self.stats["swap_outs"] += 1
-        self.stats["kernel_launches"] += 1 if self.swap_mode == L.SWAP_KERNEL else 0
+        self.stats["kernel_launches"] += 0 if self.swap_mode == L.SWAP_DMA else 1
 
     def swap_out_done(self, state) -> None:
         """Transition 4: blocks return to the pool, fenced on the gather."""
@@ -205,7 +205,7 @@ class KvDataPath:
         self._fences.append(s1)
         self.stats["swap_in_bytes"] += n * self.pool.bytes_per_token
         self.stats["swap_ins"] += 1
-        self.stats["kernel_launches"] += 1 if self.swap_mode == L.SWAP_KERNEL else 0
+        self.stats["kernel_launches"] += 0 if self.swap_mode == L.SWAP_DMA else 1
 
     def swap_in_done(self, state) -> None:
         """Transition 6: the slot can go once the scatter has read it."""

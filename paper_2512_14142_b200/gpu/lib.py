@@ -23,6 +23,7 @@ LIB_PATH = Path(os.environ.get("ASTRAEA_LIB", Path(__file__).resolve().parent.pa
 
 SWAP_KERNEL = 0
 SWAP_DMA = 1
+SWAP_STAGED = 2
 EPI_NONE = 0
 EPI_RESIDUAL = 1
 

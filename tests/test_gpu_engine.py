@@ -23,7 +23,7 @@ SCENARIOS = ["fig2/fcfs", "c1/stateful-mlfq/12000/adaptive", "c1b200/6000", "het
 
 
 @pytest.mark.parametrize("name", SCENARIOS)
-@pytest.mark.parametrize("swap_mode", [0])
+@pytest.mark.parametrize("swap_mode", [2])   # the default: staged
 def test_model_clock_report_matches_reference(name, swap_mode, golden):
     wl, pol, pred, mem, cfg = scenarios.build(host, name)
     dp = datapath_for(mem.capacity_tokens, swap_mode=swap_mode)
@@ -36,10 +36,11 @@ def test_model_clock_report_matches_reference(name, swap_mode, golden):
     assert dev["discards"] == decisions.get("discard:estimated", 0) + decisions.get("discard:deadlock-evicted", 0)
 
 
-def test_dma_swap_mode_engine():
+@pytest.mark.parametrize("swap_mode", [0, 1])   # zero-copy SM kernel, per-block 2-D DMA
+def test_other_swap_modes_engine(swap_mode):
     name = "c1b200/3600"
     wl, pol, pred, mem, cfg = scenarios.build(host, name)
-    dp = datapath_for(mem.capacity_tokens, swap_mode=1)
+    dp = datapath_for(mem.capacity_tokens, swap_mode=swap_mode)
     rep = GpuEngine(wl, pol, pred, mem, cfg, dp).run()
     assert rep.device["swap_ins"] > 100 and rep.device["free_blocks"] == rep.device["num_blocks"]
 

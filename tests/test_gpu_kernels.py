@@ -33,7 +33,7 @@ def make_pool(nb, Lyr, Hkv, D, seed=0):
 
 # ---------------------------------------------------------------- K1 / K2 swap
 
-@pytest.mark.parametrize("mode", [L.SWAP_KERNEL, L.SWAP_DMA])
+@pytest.mark.parametrize("mode", [L.SWAP_KERNEL, L.SWAP_DMA, L.SWAP_STAGED])
 @pytest.mark.parametrize("Lyr,Hkv,D,n_tokens", [(4, 2, 64, 1), (4, 2, 64, 17), (4, 2, 64, 300),
                                                 (32, 8, 128, 1000), (80, 1, 128, 129)])
 def test_swap_out_matches_oracle_and_round_trips_bit_exact(mode, Lyr, Hkv, D, n_tokens):
