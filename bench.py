@@ -76,6 +76,9 @@ def parse(argv=None):
     ap.add_argument("--cost-tables", choices=("calibrated", "b200-like", "reference"), default="calibrated",
                     help="scheduler cost tables: measured on the B200 (profiles/r1_b200_cost_tables.json), "
                          "the survey's B200-like guess, or the reference defaults")
+    ap.add_argument("--placement", choices=("free-tokens", "round-robin"), default="free-tokens",
+                    help="multi-GPU: requests placed at arrival on the replica with the most free KV "
+                         "tokens (the global scheduler, cluster.py), or round-robin over (arrival, id)")
     ap.add_argument("--measured-runs", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
@@ -107,7 +110,6 @@ def build_workload(args, rank, world):
         duration *= 2
     full = full[:need]
     full.sort(key=lambda r: (r.arrival_time, r.id))
-    shard = full[rank::world]
     tables = getattr(args, "cost_tables", "calibrated")
     if tables == "calibrated":
         pred, cal = scenarios.calibrated_predictor(ns)
@@ -118,6 +120,21 @@ def build_workload(args, rank, world):
     else:
         pred = ns.ServiceTimePredictor()
         args.swap_tokens_per_s = 20_000.0
+    placement = getattr(args, "placement", "round-robin")
+    if world == 1 or placement == "round-robin":
+        shard = full[rank::world]
+    else:
+        # the global scheduler (cluster.py) on the host: every rank computes
+        # the same placement by free KV tokens and replays its own replica
+        # (a replica's report is the reference run of its requests)
+        from paper_2512_14142_b200.cluster import ClusterScheduler
+
+        def make(i):
+            pol, mem, cfg = make_run(ns, None, pred, args, 131072)
+            return pol, pred, mem, cfg
+
+        placed = ClusterScheduler(ns, full, world, make, placement=placement).run().placement
+        shard = [r for r in full if placed[r.id] == rank]
     return shard, pred
 
 
@@ -464,11 +481,12 @@ def cpu_sample_text(k, samples):
 
 def config_block(args, shard, world, batches, s):
     return {"workload": f"C2 {args.model} random-init, reference trace generate(seed 0, qps {args.qps}/rank)"
-                        f"[:{args.requests}] = {len(shard)} requests/rank, stateful-mlfq + adaptive KV, "
+                        f"[:{args.requests * world}], {len(shard)} requests on this rank, stateful-mlfq + adaptive KV, "
                         f"capacity {args.capacity} tok/GPU, parallel-max, model clock, {args.cost_tables} "
                         f"cost tables; step = one scheduled batch, window = batches {s}..{s + args.steps - 1} "
                         f"of {len(batches)}",
-            "global_requests": len(shard) * world, "parallelism": f"replicas x{world}",
+            "global_requests": args.requests * world, "parallelism": f"replicas x{world}",
+            "placement": "single replica" if world == 1 else f"{args.placement} (cluster.py)",
             "l2": "weights (15 GB) stream every decode step: inputs >> L2 (126 MB)",
             "replay_batches": len(batches), "window_start": s, "swap_mode": args.swap_mode}
 
@@ -659,8 +677,8 @@ def main():
                      "algorithmic_bytes_per_launch": chain_bytes, "launch_ms": chain_ms,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, copy burst)"},
         "window": win,
-        "replay": {"requests": len(shard) * world, "device_ms": replay_ms,
-                   "req_per_s": len(shard) * world / (replay_ms / 1000.0), "batches": len(batches),
+        "replay": {"requests": args.requests * world, "device_ms": replay_ms,
+                   "req_per_s": args.requests * world / (replay_ms / 1000.0), "batches": len(batches),
                    "decode_steps": sum(b["decode_steps"] for b in batches),
                    "mean_decode_batch": sum(b["row_steps"] for b in batches) / max(1, sum(b["decode_steps"]
                                                                                         for b in batches))},
@@ -679,10 +697,33 @@ def main():
         line["clocks"] = clk
     if rank == 0:
         line["reference_scheduler"] = reference_scheduler(ns, shard, pred, args, cfg.kv_bytes_per_token)
+        if world > 1:
+            line["cluster"] = cluster_outcome(ns, args, world, pred, cfg.kv_bytes_per_token)
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(cfg, batches, s, min(args.steps, 3))
         print(json.dumps(line))
     barrier(world)
+
+
+def cluster_outcome(ns, args, world, pred, bytes_per_token):
+    """Whole-cluster avg / p99 JCT and req/s of the global schedule on the
+    model clock (every rank executed its replica's batches of exactly this
+    schedule), next to round-robin placement."""
+    from paper_2512_14142_b200.cluster import ClusterScheduler
+    full = []
+    rr = argparse.Namespace(**dict(vars(args), placement="round-robin"))
+    for r in range(world):
+        full += build_workload(rr, r, world)[0]
+
+    def make(i):
+        pol, mem, cfg = make_run(ns, None, pred, args, bytes_per_token)
+        return pol, pred, mem, cfg
+
+    out = {}
+    for rule in (args.placement, "round-robin"):
+        agg = ClusterScheduler(ns, full, world, make, placement=rule).run().aggregates()
+        out[rule] = {k: agg[k] for k in ("avg_jct", "p99_jct", "req_per_s", "per_replica")}
+    return {"placement": args.placement, "clock": "model", **out}
 
 
 def cpu_baseline(cfg, batches, s, k):

@@ -3,9 +3,13 @@
 The reference runs ONE engine over one memory model (simulator.py:101-481)
 and lists cross-GPU placement as a non-goal. This module gives
 N replicas -- one B200 each -- one scheduling view: every request is placed
-at its arrival instant on the replica with the most free KV tokens
-(``MemoryModel.free_tokens``, kvcache.py:110-112; ties: fewer unfinished
-requests, then the lower replica index), and from then on it is scheduled by
+at its arrival instant on the replica with the most free KV tokens net of
+commitments -- ``MemoryModel.free_tokens`` (kvcache.py:110-112) minus the
+``kv_demand`` (scheduler.py:123-132) of the replica's unfinished requests,
+i.e. the caches it must still bring back from the host, recompute or grow
+(ties: fewer unfinished requests, then the lower replica index; plain free
+tokens let a replica whose caches sit swapped out look empty and pile up
+requests, tools/placement_probe.py) -- and from then on it is scheduled by
 that replica's own, unmodified reference policy, KV policy and memory model.
 
 The replicas advance in lockstep on one virtual clock, so a placement sees
@@ -39,7 +43,7 @@ from typing import Callable, Optional, Sequence
 
 from . import reference
 
-PLACEMENTS = ("free-tokens", "round-robin")
+PLACEMENTS = ("free-tokens", "least-requests", "round-robin")
 
 
 def _step_class(base):
@@ -211,10 +215,17 @@ class ClusterScheduler:
             self._rr += 1
             return k
 
+        kv_demand = self.ns.scheduler.kv_demand
+
         def key(i):
             eng = self.replicas[i]
-            unfinished = sum(1 for st in eng.states.values() if not st.done)
-            return (-eng.memory.free_tokens, unfinished, i)
+            live = [st for st in eng.states.values() if not st.done]
+            # free tokens net of what the replica's unfinished requests must
+            # still make resident (swapped-out, dropped and queued caches)
+            free = eng.memory.free_tokens - sum(kv_demand(st) for st in live)
+            if self.placement_rule == "least-requests":
+                return (len(live), -free, i)
+            return (-free, len(live), i)
 
         return min(range(len(self.replicas)), key=key)
 
