@@ -197,7 +197,9 @@ __device__ __forceinline__ void attn_pages(const PageSrc& A, int pa, int pb, int
   }
 }
 
-constexpr int kAttnWarpBytes = kAttnBT * 128 * 2;   // per attention warp: one V page (D <= 128)
+// per attention warp: one V page (D <= 128), reused after the page loop for
+// the warp's merge state ([G] m, [G] l, [G][D] o fp32: 4,160 B at G = 8, D = 128)
+constexpr int kAttnWarpBytes = kAttnBT * 128 * 2 + 128;
 
 __device__ __forceinline__ unsigned long long tagged(float v, unsigned tag) {
   return (unsigned long long)__float_as_uint(v) | ((unsigned long long)tag << 32);

@@ -63,7 +63,7 @@ constexpr int kEpiThreads = 128;
 #endif
 constexpr int kRingBytes = MK_RING_KB * 1024;
 constexpr int kBT = 16;
-constexpr int kAttnSmem = kBT * 128 * 2;   // per attention warp: one V page (D <= 128), bf16
+constexpr int kAttnSmem = attn::kAttnWarpBytes;   // per attention warp: one V page (D <= 128) + merge room
 
 enum { PK_GEMM = 0, PK_ATTN = 1 };
 

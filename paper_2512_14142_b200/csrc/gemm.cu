@@ -853,6 +853,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         unsigned long long* atr = (tr && ew == 0) ? tr + 16 : nullptr;
         if (args.attn_kind[0] == 1) attn::attn_cta_phase<128, 4>(aw, cta, G, ew, lane, vs_all, wait_prev, done, atr);
         else if (args.attn_kind[0] == 2) attn::attn_cta_phase<64, 2>(aw, cta, G, ew, lane, vs_all, wait_prev, done);
+        else if (args.attn_kind[0] == 4) attn::attn_cta_phase<128, 8>(aw, cta, G, ew, lane, vs_all, wait_prev, done);
         else attn::attn_cta_phase<64, 4>(aw, cta, G, ew, lane, vs_all, wait_prev, done);
         pdl_wait();
         asm volatile("fence.proxy.async;" ::: "memory");
@@ -897,6 +898,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
           unsigned long long* atr = (tr && ew == 0 && k == 0) ? tr + 16 : nullptr;
           if (args.attn_kind[k] == 1) attn::attn_cta_phase<128, 4>(aw, cta, G, ew, lane, vs_all, no_wait, done, atr);
           else if (args.attn_kind[k] == 2) attn::attn_cta_phase<64, 2>(aw, cta, G, ew, lane, vs_all, no_wait, done);
+          else if (args.attn_kind[k] == 4) attn::attn_cta_phase<128, 8>(aw, cta, G, ew, lane, vs_all, no_wait, done);
           else attn::attn_cta_phase<64, 4>(aw, cta, G, ew, lane, vs_all, no_wait, done);
           asm volatile("fence.proxy.async;" ::: "memory");
           epi_bar();
@@ -930,7 +932,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
           // the next layer's attention (next launch) reads these pages: warm L2 now
           attn::AttnWork nx = args.at[args.nattn - 1];
           nx.layer = args.pf_layer;
-          if (args.attn_kind[0] == 1) attn::attn_cta_prefetch<128>(nx, cta, G, warp - 2, lane);
+          if (args.attn_kind[0] == 1 || args.attn_kind[0] == 4) attn::attn_cta_prefetch<128>(nx, cta, G, warp - 2, lane);
           else attn::attn_cta_prefetch<64>(nx, cta, G, warp - 2, lane);
         }
       }
@@ -1127,7 +1129,7 @@ SkPlan sk_plan(int M, int N, int K) {
 constexpr size_t kCounterBytes = 16384 * sizeof(int);
 constexpr size_t kPhaseBytes = 256;
 // attention phase of a layer chain: [grid <= 192][G <= 4][D + 2 <= 130] tagged split partials
-constexpr size_t kAttnWsBytes = (size_t)192 * 4 * 130 * sizeof(unsigned long long);
+constexpr size_t kAttnWsBytes = (size_t)192 * 8 * 130 * sizeof(unsigned long long);   // grid x G x (D + 2), G*D <= 1024
 constexpr size_t kHeadBytes = kCounterBytes + kPhaseBytes + kAttnWsBytes;   // before the GEMM partials
 
 size_t partial_bytes(int M, const SkPlan& p) { return (size_t)p.tiles * p.maxseg * M * kBM * sizeof(unsigned long long); }
@@ -1388,7 +1390,8 @@ static int run_chain(int M, int nph, const astraea_gemm_phase* ph, void* ws, siz
         (k && attn_before[k] <= attn_before[k - 1]))
       return ASTRAEA_EINVAL;
     const int G = at->num_q_heads / g.num_kv_heads, D = g.head_dim;
-    a.attn_kind[k] = (D == 128 && G == 4) ? 1 : (D == 64 && G == 2) ? 2 : (D == 64 && G == 4) ? 3 : 0;
+    a.attn_kind[k] = (D == 128 && G == 4) ? 1 : (D == 64 && G == 2) ? 2 : (D == 64 && G == 4) ? 3
+                   : (D == 128 && G == 8) ? 4 : 0;   // 4: a Llama-3-70B TP=8 rank (8 q heads on 1 kv head)
     if (!a.attn_kind[k] || num_sms() > 192) return ASTRAEA_EUNSUPPORTED;
     a.attn_before[k] = attn_before[k];
     attn::AttnWork& w = a.at[k];

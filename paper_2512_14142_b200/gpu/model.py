@@ -394,7 +394,7 @@ class LlamaRunner:
     def _attn_fusable(self) -> bool:
         cfg = self.cfg
         G = cfg.num_q_heads // cfg.num_kv_heads
-        return (cfg.head_dim, G) in ((128, 4), (64, 2), (64, 4))
+        return (cfg.head_dim, G) in ((128, 4), (64, 2), (64, 4), (128, 8))
 
     def _step_supported(self) -> bool:
         cfg = self.cfg

@@ -70,16 +70,31 @@ class TpLlamaRunner(LlamaRunner):
                  max_rows: int = 64):
         super().__init__(weights, pool, max_tokens=max_tokens, max_rows=max_rows)
         self.rank, self.world, self.group = rank, world, group
-        self.use_chain = False
+        self.use_chain = True     # decode: two chained launches per layer around the all-reduces
         self.use_step_kernel = False
         self.hidden = weights.embed.shape[1]
 
-    def _allreduce(self, t, op=None):
+    def _allreduce(self, t, op=None, stream=None):
+        """In-place all-reduce of ``t``, ordered on ``stream`` (the stream the
+        kernels producing and consuming ``t`` run on): torch.distributed
+        enqueues on the current stream."""
         if self.world == 1:
             return t
+        import contextlib
+
         import torch.distributed as dist
-        dist.all_reduce(t, op=op or dist.ReduceOp.SUM, group=self.group)
+        ctx = torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+        with ctx:
+            dist.all_reduce(t, op=op or dist.ReduceOp.SUM, group=self.group)
         return t
+
+    def _residual_pair(self, T, dev):
+        """Ping-pong buffers for the replicated residual stream: a projection
+        writes its partial sums (rank 0: + residual) into the buffer the
+        residual does not occupy, the all-reduce runs in place there, and that
+        buffer becomes the residual -- no copy after a collective."""
+        d = self.hidden
+        return [torch.empty(T, d, dtype=torch.bfloat16, device=dev) for _ in range(2)]
 
     def _layers(self, x, ssq, positions, slots, attend, stream=None):
         cfg, w, pool = self.cfg, self.w, self.pool
@@ -90,7 +105,7 @@ class TpLlamaRunner(LlamaRunner):
         q = torch.empty(T, qd, dtype=torch.bfloat16, device=dev)
         att = torch.empty(T, qd, dtype=torch.bfloat16, device=dev)
         h = torch.empty(T, cfg.ffn, dtype=torch.bfloat16, device=dev)
-        part = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+        pair = self._residual_pair(T, dev)
         ws = self.gemm_ws
         cs = ops.rope_table(positions, cfg.head_dim, cfg.rope_theta, stream=stream)
         lead = self.rank == 0
@@ -99,15 +114,17 @@ class TpLlamaRunner(LlamaRunner):
                         geo=pool.geo, layer=li, num_q_heads=cfg.num_q_heads, positions=positions, slots=slots,
                         rope_theta=cfg.rope_theta, rope_table=cs, workspace=ws, stream=stream)
             attend(li, q, att)
+            part = pair[1] if x is pair[0] else pair[0]
             ops.gemm_ex(att, lw["wo"], part, kind=L.EPI_RESIDUAL if lead else L.EPI_NONE,
                         residual=x if lead else None, workspace=ws, stream=stream)
-            x = self._allreduce(part).clone() if self.world > 1 else part.clone()
+            x = self._allreduce(part, stream=stream)
             ssq_mid = ops.row_ssq(x, stream=stream)
             ops.gemm_ex(x, lw["wgu"], h, kind=L.EPI_SILU, ssq_in=ssq_mid, rms_dim=d, rms_eps=eps, workspace=ws,
                         stream=stream)
+            part = pair[1] if x is pair[0] else pair[0]
             ops.gemm_ex(h, lw["wdown"], part, kind=L.EPI_RESIDUAL if lead else L.EPI_NONE,
                         residual=x if lead else None, workspace=ws, stream=stream)
-            x = self._allreduce(part).clone() if self.world > 1 else part.clone()
+            x = self._allreduce(part, stream=stream)
             ssq = ops.row_ssq(x, stream=stream)
         return x, ssq
 
@@ -122,19 +139,63 @@ class TpLlamaRunner(LlamaRunner):
                     rms_eps=cfg.eps, argmax_keys=keys, argmax_col_offset=self.rank * cfg.vocab,
                     workspace=self.gemm_ws, stream=stream)
         if self.world > 1:
-            # keys are order-preserving unsigned (value, ~column) pairs: as int64 they compare like the
-            # unsigned keys only when the top bit agrees, so reduce the bit-flipped signed view
-            flipped = keys ^ torch.iinfo(torch.int64).min
-            self._allreduce(flipped, op=dist.ReduceOp.MAX)
-            keys.copy_(flipped ^ torch.iinfo(torch.int64).min)
-            if want_logits:
-                parts = [torch.empty_like(logits) for _ in range(self.world)]
-                dist.all_gather(parts, logits, group=self.group)
-                logits = torch.cat(parts, dim=1)
+            import contextlib
+            ctx = torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+            with ctx:   # the key and logits exchange run on the kernels' stream
+                # keys are order-preserving unsigned (value, ~column) pairs: as int64 they compare like
+                # the unsigned keys only when the top bit agrees, so reduce the bit-flipped signed view
+                flipped = keys ^ torch.iinfo(torch.int64).min
+                dist.all_reduce(flipped, op=dist.ReduceOp.MAX, group=self.group)
+                keys.copy_(flipped ^ torch.iinfo(torch.int64).min)
+                if want_logits:
+                    parts = [torch.empty_like(logits) for _ in range(self.world)]
+                    dist.all_gather(parts, logits, group=self.group)
+                    logits = torch.cat(parts, dim=1)
         if keys_out is not None:
             return (keys_out, logits) if want_logits else keys_out
         ids = ops.keys_to_ids(keys)
         return (ids, logits) if want_logits else ids
 
     def decode(self, tokens, positions, slots, table, ctx, stream=None, want_logits=False, keys_out=None):
-        return self._decode_unchained(tokens, positions, slots, table, ctx, stream, want_logits, keys_out)
+        """One decode step of this rank: per layer two chained launches around
+        the two all-reduces -- [QKV (RoPE + KV append) -> paged attention ->
+        O partials] and [gate/up -> down partials] -- each partial written
+        straight into the buffer the all-reduce then reduces in place; the
+        RMSNorm statistics of the reduced residual come from one row_ssq."""
+        if not self.use_chain or not self._attn_fusable() or tokens.shape[0] > 64:
+            return self._decode_unchained(tokens, positions, slots, table, ctx, stream, want_logits, keys_out)
+        cfg, w, pool = self.cfg, self.w, self.pool
+        B = tokens.shape[0]
+        dev = tokens.device
+        d, eps = self.hidden, cfg.eps
+        qd = cfg.num_q_heads * cfg.head_dim
+        x, ssq = self._embed(tokens, stream)
+        q = torch.empty(B, qd, dtype=torch.bfloat16, device=dev)
+        att = torch.empty(B, qd, dtype=torch.bfloat16, device=dev)
+        h = torch.empty(B, cfg.ffn, dtype=torch.bfloat16, device=dev)
+        pair = self._residual_pair(B, dev)
+        ws = self.gemm_ws
+        cs = ops.rope_table(positions, cfg.head_dim, cfg.rope_theta, stream=stream)
+        lead = self.rank == 0
+        for li, lw in enumerate(w.layers):
+            part = pair[1] if x is pair[0] else pair[0]
+            ops.gemm_chain([
+                dict(a=x, w=lw["wqkv"], out=q, kind=L.EPI_QKV_ROPE, ssq_in=ssq, rms_dim=d, rms_eps=eps,
+                     pool=pool.data, geo=pool.geo, layer=li, num_q_heads=cfg.num_q_heads, positions=positions,
+                     slots=slots, rope_theta=cfg.rope_theta, rope_table=cs),
+                dict(a=att, w=lw["wo"], out=part, kind=L.EPI_RESIDUAL if lead else L.EPI_NONE,
+                     residual=x if lead else None),
+            ], ws, stream=stream, attn=[dict(pool=pool.data, geo=pool.geo, layer=li, num_q_heads=cfg.num_q_heads,
+                                             q=q, q_stride=qd, table=table, ctx=ctx, scale=self.scale, out=att,
+                                             before=1)])
+            x = self._allreduce(part, stream=stream)
+            ssq_mid = ops.row_ssq(x, stream=stream)
+            part = pair[1] if x is pair[0] else pair[0]
+            ops.gemm_chain([
+                dict(a=x, w=lw["wgu"], out=h, kind=L.EPI_SILU, ssq_in=ssq_mid, rms_dim=d, rms_eps=eps),
+                dict(a=h, w=lw["wdown"], out=part, kind=L.EPI_RESIDUAL if lead else L.EPI_NONE,
+                     residual=x if lead else None),
+            ], ws, stream=stream)
+            x = self._allreduce(part, stream=stream)
+            ssq = ops.row_ssq(x, stream=stream)
+        return self._sample(x, ssq, stream, want_logits, keys_out)
