@@ -44,6 +44,7 @@ struct DecodeParams {
   long long block_el;  // elements per pool block
   int layer, Hkv, Hq, max_blocks, blocks_per_split, splits;
   float scale_log2;
+  int block_rows;  // TMA path: rows of one pool block in the [blocks x L x 2 x Hkv x 16][D] view
 };
 
 // Warp-per-tile decode attention. Each of the 4 warps owns a private 2-deep
@@ -320,30 +321,18 @@ constexpr int decode_mma_warp_bytes() {   // a V page, or the warp's merged stat
   return kBT * D * 2 > (2 * G + G * D) * 4 ? kBT * D * 2 : (2 * G + G * D) * 4;
 }
 
+// Shared tail of the tensor-core decode kernels: merge the 4 warps' states
+// (warp order) through shared memory (each warp's region of wreg bf16
+// elements is free once its page loop is done), then either write the
+// output (one split) or the split partial, the last split CTA merging all
+// splits in split order.
 template <int D, int G>
-__global__ void __launch_bounds__(128) decode_mma_kernel(const __grid_constant__ DecodeParams p) {
-  using namespace astraea::attn;
+__device__ __forceinline__ void decode_merge_tail(const DecodeParams& p, bf16* vs_all, int wreg,
+                                                  const astraea::attn::AttnAcc<D>& st, int b, int h,
+                                                  int split, int tid, int warp, int lane) {
   constexpr int EPT = (G * D + 127) / 128;
-  constexpr int WREG = decode_mma_warp_bytes<D, G>() / 2;   // per-warp region (bf16 elements)
-  extern __shared__ __align__(128) uint8_t dsm[];
-  bf16* vs_all = reinterpret_cast<bf16*>(dsm);   // [4][WREG]: V page, then the warp's state
-  const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  pdl_wait();
-  pdl_launch();
-  const int ctx = p.ctx[b];
-  const int nblk = (ctx + kBT - 1) / kBT;
-  const int b0 = split * p.blocks_per_split;
-  const int b1 = min(nblk, b0 + p.blocks_per_split);
   const int r8 = lane >> 2, quad = lane & 3;
-  uint32_t qa[D / 8];
-  attn_load_q<D>(p.q + (long long)b * p.q_stride + (long long)(h * G + r8) * D, r8 < G, quad, qa);
-  const PageSrc src = page_src<D>(p.pool, p.block_el, p.layer, p.Hkv, h, p.table + (long long)b * p.max_blocks,
-                                  p.scale_log2);
-  bf16* vs = vs_all + warp * WREG;
-  AttnAcc<D> st;
-  attn_pages<D>(src, b0 + warp, b1, 4, ctx, qa, vs, st, lane);
-  // merge the 4 warps (warp order) through shared memory
+  bf16* vs = vs_all + warp * wreg;
   float* wst = reinterpret_cast<float*>(vs);   // [G] m, [G] l, [G][D] o (the warp's V page is free now)
   __syncwarp();
   if (r8 < G) {
@@ -366,7 +355,7 @@ __global__ void __launch_bounds__(128) decode_mma_kernel(const __grid_constant__
     if (idx < G * D) {
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
-        const float* ws = reinterpret_cast<const float*>(vs_all + w * WREG);
+        const float* ws = reinterpret_cast<const float*>(vs_all + w * wreg);
         const float mk = ws[g], mn = fmaxf(Mv[e], mk);
         const float a0 = mn == -INFINITY ? 0.f : exp2f(Mv[e] - mn), a1 = mn == -INFINITY ? 0.f : exp2f(mk - mn);
         Lv[e] = Lv[e] * a0 + ws[G + g] * a1;
@@ -440,6 +429,79 @@ __global__ void __launch_bounds__(128) decode_mma_kernel(const __grid_constant__
     p.out[(bh0 + g) * D + dd] = f2bf(den > 0.f ? num / den : 0.f);
   }
   if (tid == 0) *ctr = 0;
+}
+
+template <int D, int G>
+__global__ void __launch_bounds__(128) decode_mma_kernel(const __grid_constant__ DecodeParams p) {
+  using namespace astraea::attn;
+  constexpr int WREG = decode_mma_warp_bytes<D, G>() / 2;   // per-warp region (bf16 elements)
+  extern __shared__ __align__(128) uint8_t dsm[];
+  bf16* vs_all = reinterpret_cast<bf16*>(dsm);   // [4][WREG]: V page, then the warp's state
+  const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  pdl_wait();
+  pdl_launch();
+  const int ctx = p.ctx[b];
+  const int nblk = (ctx + kBT - 1) / kBT;
+  const int b0 = split * p.blocks_per_split;
+  const int b1 = min(nblk, b0 + p.blocks_per_split);
+  const int r8 = lane >> 2, quad = lane & 3;
+  uint32_t qa[D / 8];
+  attn_load_q<D>(p.q + (long long)b * p.q_stride + (long long)(h * G + r8) * D, r8 < G, quad, qa);
+  const PageSrc src = page_src<D>(p.pool, p.block_el, p.layer, p.Hkv, h, p.table + (long long)b * p.max_blocks,
+                                  p.scale_log2);
+  bf16* vs = vs_all + warp * WREG;
+  AttnAcc<D> st;
+  attn_pages<D>(src, b0 + warp, b1, 4, ctx, qa, vs, st, lane);
+  decode_merge_tail<D, G>(p, vs_all, WREG, st, b, h, split, tid, warp, lane);
+}
+
+// ---------------------------------------------------------------------------
+// K4 for the larger batches: the same tensor-core page math, but every warp
+// keeps S pages in flight. K and V pages arrive by TMA (a 2-D tensor map over
+// the pool viewed as [pages x 16 rows][D], 128-byte swizzle, one box of 16
+// rows x 64 columns per half page) into a per-warp ring of S stages with one
+// mbarrier each; the warp computes page k while pages k+1..k+S-1 are in
+// flight, and lane 0 refills the stage as soon as the warp has read it. The
+// swizzle keeps the ldmatrix reads of K (scores) and V (transposed, PV)
+// conflict-free. With S = 3 and 96 KB per CTA, two CTAs per SM keep up to
+// 24 pages (192 KB) per SM in flight -- what HBM latency x per-SM bandwidth
+// asks for -- where the one-page-per-warp walk keeps ~32 KB.
+// ---------------------------------------------------------------------------
+template <int D, int G, int S>
+__global__ void __launch_bounds__(128) decode_tma_kernel(const __grid_constant__ CUtensorMap pool_map,
+                                                         const __grid_constant__ DecodeParams p) {
+  using namespace astraea::attn;
+  constexpr int PB = tma_page_bytes<D>();
+  extern __shared__ __align__(1024) uint8_t dsm_raw[];
+  uint8_t* dsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t bar[4 * S];
+  const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (lane < S) mbar_init(&bar[warp * S + lane], 1);
+  fence_barrier_init();
+  __syncwarp();
+  if (tid == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&pool_map) : "memory");
+  pdl_wait();
+  pdl_launch();
+  const int ctx = p.ctx[b];
+  const int nblk = (ctx + kBT - 1) / kBT;
+  const int b0 = split * p.blocks_per_split;
+  const int b1 = min(nblk, b0 + p.blocks_per_split);
+  const int r8 = lane >> 2, quad = lane & 3;
+  uint32_t qs[D / 16][2];
+  attn_load_q_std<D>(p.q + (long long)b * p.q_stride + (long long)(h * G + r8) * D, r8 < G, quad, qs);
+  TmaPages T;
+  T.map = &pool_map;
+  T.block_rows = p.block_rows;
+  T.k_row0 = (p.layer * 2 * p.Hkv + h) * kBT;
+  T.v_row0 = T.k_row0 + p.Hkv * kBT;
+  AttnAcc<D> st;
+  uint32_t cnt = 0;
+  attn_pages_tma<D, S>(T, p.table + (long long)b * p.max_blocks, b0 + warp, b1, 4, ctx, p.scale_log2, qs,
+                       dsm + (size_t)warp * S * PB, &bar[warp * S], cnt, st, lane);
+  // the merge reuses each warp's ring (all of its pages have landed and been read)
+  decode_merge_tail<D, G>(p, reinterpret_cast<bf16*>(dsm), S * PB / 2, st, b, h, split, tid, warp, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -665,13 +727,14 @@ __global__ void __launch_bounds__(128) prefill_kernel(const __grid_constant__ Pr
   }
 }
 
-int decode_splits(int B, int Hkv, int max_blocks, int* bps) {
+int decode_splits(int B, int Hkv, int max_blocks, int* bps, int min_blocks = 0) {
   // Enough CTAs to cover the SMs, but at least kMinBlocks blocks (8 KiB of
   // K+V per head per block) per CTA so per-CTA fixed costs stay small.
-  static const int kMinBlocks = [] {
+  static const int kEnvMin = [] {
     const char* e = getenv("ASTRAEA_DECODE_MIN_BLOCKS");
     return e ? std::max(1, atoi(e)) : 8;
   }();
+  const int kMinBlocks = min_blocks > 0 ? min_blocks : kEnvMin;
   const int target = 2 * num_sms();
   const int base = B * Hkv;
   int want = (target + base - 1) / base;
@@ -751,10 +814,48 @@ extern "C" int astraea_paged_decode_attention(const astraea_kv_geometry* g, cons
     constexpr size_t smem = 4 * decode_mma_warp_bytes<DD, GG>();                                   \
     ASTRAEA_TRY(launch_k(decode_mma_kernel<DD, GG>, grid, dim3(128), smem, st, p));                 \
   } while (0)
-  static const bool use_mma = [] {
+#define LAUNCH_TMA(DD, GG)                                                                         \
+  do {                                                                                               \
+    constexpr int S = 3;                                                                             \
+    constexpr size_t smem = 1024 + (size_t)4 * S * astraea::attn::tma_page_bytes<DD>();             \
+    static bool attr = false;                                                                        \
+    if (!attr) {                                                                                     \
+      ASTRAEA_TRY(cudaFuncSetAttribute(decode_tma_kernel<DD, GG, S>,                                 \
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));     \
+      attr = true;                                                                                   \
+    }                                                                                                \
+    ASTRAEA_TRY(launch_k(decode_tma_kernel<DD, GG, S>, grid, dim3(128), smem, st, map, p));         \
+  } while (0)
+  static const char mode = [] {
     const char* e = getenv("ASTRAEA_DECODE_ATTN");
-    return !(e && e[0] == 's');   // "simt": the CUDA-core kernel
+    return e ? e[0] : 't';   // 't' TMA-staged (default), 'm' one page per warp, 's' CUDA cores
   }();
+  const bool use_mma = mode != 's';
+  if (mode == 't' && D * 2 <= 256 && (D == 128 || D == 64)) {
+    // TMA-staged kernel: its own split (each warp >= S pages: 12 blocks per split)
+    int bps2 = 0;
+    const int sp2 = decode_splits(B, Hkv, max_blocks, &bps2, 12);
+    const bool ok_g = (D == 128 && (G == 4 || G == 8)) || (D == 64 && (G == 2 || G == 4));
+    if (sp2 > 0 && ok_g) {
+      const size_t need2 = kDecCounterBytes + (size_t)B * Hq * sp2 * (D + 1) * sizeof(float);
+      if (sp2 > 1 && (!ws || ws_bytes < need2)) return ASTRAEA_EINVAL;
+      p.splits = sp2;
+      p.blocks_per_split = bps2;
+      p.ws_lse = p.ws_o + (size_t)B * Hq * p.splits * D;
+      p.block_rows = g->num_layers * 2 * Hkv * kBT;
+      CUtensorMap map;
+      int rc = astraea::tc::make_map(&map, pool, (long long)g->num_blocks * p.block_rows, D, D, kBT);
+      if (rc) return rc;
+      dim3 grid2(p.splits, Hkv, B);
+      grid = grid2;
+      if (D == 128 && G == 4) LAUNCH_TMA(128, 4);
+      else if (D == 128 && G == 8) LAUNCH_TMA(128, 8);
+      else if (D == 64 && G == 4) LAUNCH_TMA(64, 4);
+      else LAUNCH_TMA(64, 2);
+      ASTRAEA_CHECK_LAUNCH();
+      return ASTRAEA_OK;
+    }
+  }
   if (use_mma && D == 128 && G == 4) LAUNCH_MMA(128, 4);
   else if (use_mma && D == 128 && G == 8) LAUNCH_MMA(128, 8);
   else if (use_mma && D == 64 && G == 4) LAUNCH_MMA(64, 4);
@@ -769,6 +870,7 @@ extern "C" int astraea_paged_decode_attention(const astraea_kv_geometry* g, cons
   else return ASTRAEA_EUNSUPPORTED;
 #undef LAUNCH_DEC
 #undef LAUNCH_MMA
+#undef LAUNCH_TMA
   ASTRAEA_CHECK_LAUNCH();
   return ASTRAEA_OK;
 }

@@ -197,6 +197,140 @@ __device__ __forceinline__ void attn_pages(const PageSrc& A, int pa, int pb, int
   }
 }
 
+// ---------------------------------------------------------------------------
+// The same page math with S pages in flight per warp (S >= 2): K and V pages
+// arrive by TMA -- a 2-D tensor map over the pool viewed as
+// [blocks x L x 2 x Hkv x 16 rows][D], 128-byte swizzle, one 16-row x
+// 64-column box per half page -- into the warp's ring of S stages (one
+// mbarrier each). The warp computes page k while pages k+1..k+S-1 land; lane
+// 0 refills a stage as soon as the warp has read it. The swizzle keeps the
+// ldmatrix reads of K (scores) and V (transposed, PV) conflict-free. Q is in
+// the standard A-fragment layout (attn_load_q_std). ``cnt``: the warp's
+// running page count (ring position and barrier phase), carried across
+// pieces and launches' phases.
+// ---------------------------------------------------------------------------
+template <int D>
+constexpr int tma_page_bytes() { return 2 * kAttnBT * D * 2; }   // K + V page
+
+__device__ __forceinline__ uint32_t sw128_off(int row, int chunk) {   // in [16 rows][64 cols] half pages
+  return (uint32_t)((chunk >> 3) * (kAttnBT * 128) + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
+}
+
+template <int D>
+__device__ __forceinline__ void attn_load_q_std(const bf16* q_row, bool ok, int quad, uint32_t (*qa)[2]) {
+#pragma unroll
+  for (int ks = 0; ks < D / 16; ++ks) {
+    qa[ks][0] = ok ? __ldcg(reinterpret_cast<const unsigned int*>(q_row + 16 * ks + 2 * quad)) : 0u;
+    qa[ks][1] = ok ? __ldcg(reinterpret_cast<const unsigned int*>(q_row + 16 * ks + 8 + 2 * quad)) : 0u;
+  }
+}
+
+struct TmaPages {
+  const CUtensorMap* map;
+  int block_rows;          // rows of one pool block in the 2-D view (L * 2 * Hkv * 16)
+  int k_row0, v_row0;      // (layer, head) row offsets of the K and V pages within a block
+};
+
+template <int D, int S>
+__device__ __forceinline__ void attn_pages_tma(const TmaPages& T, const int32_t* trow, int pa, int pb, int pstep,
+                                               int ctx_b, float scale_log2, const uint32_t (*qa)[2],
+                                               uint8_t* ring, uint64_t* bars, uint32_t& cnt, AttnAcc<D>& st,
+                                               int lane) {
+  constexpr int PB = tma_page_bytes<D>();
+  constexpr int HALF = kAttnBT * 128;
+  constexpr int KS = D / 16, NT = D / 8;
+  st.m = -INFINITY;
+  st.l = 0.f;
+#pragma unroll
+  for (int n = 0; n < NT; ++n)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) st.o[n][i] = 0.f;
+  const int my = pb > pa ? (pb - pa + pstep - 1) / pstep : 0;
+  if (my == 0) return;
+  auto ids_of = [&](int w0) { return w0 + lane < my ? __ldg(trow + pa + pstep * (w0 + lane)) : 0; };
+  int blk_c = ids_of(0), blk_n = ids_of(32);
+  auto issue = [&](int k, int blk) {   // lane 0: page k into stage (cnt + k) % S
+    const uint32_t slot = (cnt + k) % S;
+    uint64_t* bb = bars + slot;
+    uint8_t* stw = ring + slot * PB;
+    const int kr = blk * T.block_rows + T.k_row0, vr = blk * T.block_rows + T.v_row0;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the warp's reads of the stage come first
+    mbar_arrive_expect_tx(bb, PB);
+#pragma unroll
+    for (int hf = 0; hf < D / 64; ++hf) {
+      tc::tma_load_2d(stw + hf * HALF, T.map, bb, hf * 64, kr);
+      tc::tma_load_2d(stw + (D / 64) * HALF + hf * HALF, T.map, bb, hf * 64, vr);
+    }
+  };
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    const int blk = __shfl_sync(0xffffffffu, blk_c, k);
+    if (lane == 0 && k < my) issue(k, blk);
+  }
+  const int quad = lane & 3;
+  for (int k = 0; k < my; ++k) {
+    const int pg = pa + pstep * k;
+    const int n_valid = min(kAttnBT, ctx_b - pg * kAttnBT);
+    const int nxt = k + S;
+    if ((nxt & 31) == 1) blk_n = ids_of(nxt + 31);   // the next 32-page window, early
+    if ((nxt & 31) == 0) blk_c = blk_n;
+    const int nxt_blk = __shfl_sync(0xffffffffu, blk_c, nxt & 31);
+    const uint32_t slot = (cnt + k) % S;
+    mbar_wait(bars + slot, ((cnt + k) / S) & 1);
+    const uint32_t kb = smem_u32(ring + slot * PB), vb = kb + (D / 64) * HALF;
+    // S = Q K^T: ldmatrix.x4 gives (tok 0-7, k lo)(tok 0-7, k hi)(tok 8-15, k lo)(tok 8-15, k hi)
+    float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int r = (lane & 7) + ((lane >> 4) << 3);
+      const int c = 2 * ks + ((lane >> 3) & 1);
+      uint32_t b0, b1, b2, b3;
+      asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3) : "r"(kb + sw128_off(r, c)));
+      mma_16816(s0, qa[ks][0], 0u, qa[ks][1], 0u, b0, b1);
+      mma_16816(s1, qa[ks][0], 0u, qa[ks][1], 0u, b2, b3);
+    }
+    // online softmax of row lane/4 over the page (tokens 2q, 2q+1, 8+2q, 9+2q)
+    const int t0 = 2 * quad;
+    const float v00 = t0 < n_valid ? s0[0] * scale_log2 : -INFINITY;
+    const float v01 = t0 + 1 < n_valid ? s0[1] * scale_log2 : -INFINITY;
+    const float v10 = t0 + 8 < n_valid ? s1[0] * scale_log2 : -INFINITY;
+    const float v11 = t0 + 9 < n_valid ? s1[1] * scale_log2 : -INFINITY;
+    float mx = fmaxf(fmaxf(v00, v01), fmaxf(v10, v11));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float mnew = fmaxf(st.m, mx);
+    const float alpha = mnew == -INFINITY ? 1.f : exp2f(st.m - mnew);
+    const float p00 = v00 == -INFINITY ? 0.f : exp2f(v00 - mnew), p01 = v01 == -INFINITY ? 0.f : exp2f(v01 - mnew);
+    const float p10 = v10 == -INFINITY ? 0.f : exp2f(v10 - mnew), p11 = v11 == -INFINITY ? 0.f : exp2f(v11 - mnew);
+    float sum = (p00 + p01) + (p10 + p11);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    st.l = st.l * alpha + sum;
+    st.m = mnew;
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      st.o[n][0] *= alpha;
+      st.o[n][1] *= alpha;
+    }
+    const uint32_t pa0 = pack_bf2(p00, p01), pa2 = pack_bf2(p10, p11);
+    // O += P V: ldmatrix.trans of (tok 0-7, d)(tok 8-15, d)(tok 0-7, d+8)(tok 8-15, d+8)
+#pragma unroll
+    for (int m2 = 0; m2 < NT / 2; ++m2) {
+      const int r = (lane & 7) + (((lane >> 3) & 1) << 3);
+      const int c = 2 * m2 + (lane >> 4);
+      uint32_t b0, b1, b2, b3;
+      asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3) : "r"(vb + sw128_off(r, c)));
+      mma_16816(st.o[2 * m2], pa0, 0u, pa2, 0u, b0, b1);
+      mma_16816(st.o[2 * m2 + 1], pa0, 0u, pa2, 0u, b2, b3);
+    }
+    __syncwarp();
+    if (lane == 0 && nxt < my) issue(nxt, nxt_blk);   // refill this stage with page k + S
+  }
+  cnt += (uint32_t)my;
+}
+
 // per attention warp: one V page (D <= 128), reused after the page loop for
 // the warp's merge state ([G] m, [G] l, [G][D] o fp32: 4,160 B at G = 8, D = 128)
 constexpr int kAttnWarpBytes = kAttnBT * 128 * 2 + 128;
@@ -383,10 +517,14 @@ __device__ __forceinline__ void attn_cta_prefetch(const AttnWork& A, int cta, in
 // wait_head(h, lane) runs before the first q / page load (e.g. waits for the
 // kernel that produced q and the new K/V); done_head(h, thread) after the
 // merged output is written.
-template <int D, int G, class WaitHead, class DoneHead>
+// AS > 1: the TMA-staged page loop (attn_pages_tma) with AS stages per warp
+// in vs_all ([4][AS][K + V page], 1024-byte aligned), barriers abar[4][AS] and
+// the warps' running page counts acnt (caller-initialised, carried over).
+template <int D, int G, int AS = 1, class WaitHead, class DoneHead>
 __device__ __forceinline__ void attn_cta_phase(const AttnWork& A, int cta, int grid, int warp, int lane,
                                                bf16* vs_all, const WaitHead& wait_head, const DoneHead& done_head,
-                                               unsigned long long* atr = nullptr) {
+                                               unsigned long long* atr = nullptr, const TmaPages* tp = nullptr,
+                                               uint64_t* abar = nullptr, uint32_t* acnt = nullptr) {
   // atr (diagnostics, may be null): [0] entry, [1] wait_head passed, [2] q
   // loaded, [3] pages done, [4] CTA merge + partial published, [5] split
   // merge done, [6] output published, [7] exit, [8..12] first page, [13]
@@ -396,7 +534,8 @@ __device__ __forceinline__ void attn_cta_phase(const AttnWork& A, int cta, int g
   };
   mark(0);
   const int et = warp * 32 + lane;
-  bf16* vs = vs_all + warp * (kAttnWarpBytes / 2);
+  constexpr int WREG = (AS > 1 ? AS * tma_page_bytes<D>() : kAttnWarpBytes) / 2;   // per-warp region (bf16)
+  bf16* vs = vs_all + warp * WREG;
   AttnSplit sp;
   sp.init(A, cta, grid, lane);
   constexpr int EPT = (G * D + 128 - 1) / 128;   // merged elements per thread
@@ -411,13 +550,24 @@ __device__ __forceinline__ void attn_cta_phase(const AttnWork& A, int cta, int g
     mark(1);
     const int ctx_b = __ldg(A.ctx + b);
     const int r8 = lane >> 2, quad = lane & 3;
-    uint32_t qa[D / 8];
-    attn_load_q<D>(A.q + (long long)b * A.q_stride + (long long)(h * G + r8) * D, r8 < G, quad, qa);
-    mark(2);
     AttnAcc<D> st;
-    const PageSrc src = page_src<D>(A.pool, A.block_el, A.layer, A.Hkv, h, A.table + (long long)b * A.max_blocks,
-                                    A.scale_log2);
-    attn_pages<D>(src, pc.pa + warp, pc.pb, 4, ctx_b, qa, vs, st, lane, atr ? atr + 8 : nullptr);
+    if constexpr (AS > 1) {
+      uint32_t qs[D / 16][2];
+      attn_load_q_std<D>(A.q + (long long)b * A.q_stride + (long long)(h * G + r8) * D, r8 < G, quad, qs);
+      mark(2);
+      TmaPages T = *tp;
+      T.k_row0 = (A.layer * 2 * A.Hkv + h) * kAttnBT;
+      T.v_row0 = T.k_row0 + A.Hkv * kAttnBT;
+      attn_pages_tma<D, AS>(T, A.table + (long long)b * A.max_blocks, pc.pa + warp, pc.pb, 4, ctx_b, A.scale_log2,
+                            qs, reinterpret_cast<uint8_t*>(vs), abar + warp * AS, acnt[warp], st, lane);
+    } else {
+      uint32_t qa[D / 8];
+      attn_load_q<D>(A.q + (long long)b * A.q_stride + (long long)(h * G + r8) * D, r8 < G, quad, qa);
+      mark(2);
+      const PageSrc src = page_src<D>(A.pool, A.block_el, A.layer, A.Hkv, h,
+                                      A.table + (long long)b * A.max_blocks, A.scale_log2);
+      attn_pages<D>(src, pc.pa + warp, pc.pb, 4, ctx_b, qa, vs, st, lane, atr ? atr + 8 : nullptr);
+    }
     mark(3);
     // ---- CTA merge of the 4 warps' states (warp order) through shared memory
     float* wst = reinterpret_cast<float*>(vs);   // this warp's V page is free now: [G] m, [G] l, [G][D] o
@@ -442,7 +592,7 @@ __device__ __forceinline__ void attn_cta_phase(const AttnWork& A, int cta, int g
       if (idx < G * D) {
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
-          const float* ws = reinterpret_cast<const float*>(vs_all + w * (kAttnWarpBytes / 2));
+          const float* ws = reinterpret_cast<const float*>(vs_all + w * WREG);
           const float mk = ws[g], mn = fmaxf(Mv[e], mk);
           const float a0 = mn == -INFINITY ? 0.f : exp2f(Mv[e] - mn), a1 = mn == -INFINITY ? 0.f : exp2f(mk - mn);
           Lv[e] = Lv[e] * a0 + ws[G + g] * a1;

@@ -600,6 +600,7 @@ __device__ __forceinline__ void sk_range(const SkPhase& P, int cta, long long& u
 struct ChainMaps {
   CUtensorMap w[kMaxPhases];
   CUtensorMap x[kMaxPhases];
+  CUtensorMap pool;            // attention (AS > 1): the KV pool as [blocks x L x 2 x Hkv x 16][D]
 };
 
 struct ChainArgs {
@@ -615,6 +616,7 @@ struct ChainArgs {
   attn::AttnWork at[kMaxAttn];
   int pf_layer;                // >= 0: prefetch that layer's K/V pages into L2 during the last phase
   int attn_early;              // the first attention's work split runs before griddepcontrol.wait
+  int block_rows;              // attention (AS > 1): rows of one pool block in ChainMaps::pool
   SkPhase ph[kMaxPhases];
 };
 constexpr int kAttnCtr = kMaxPhases + 2;   // phase_ctr slots kAttnCtr + k: CTAs done with attention k
@@ -672,7 +674,9 @@ __device__ __forceinline__ void wait_phase(const int* ctr, int target) {
 }
 
 
-template <int BN, int STAGES, int MINB, int MT = BN>   // MT: token loops' bound (1: batch of one)
+// MT: token loops' bound (1: batch of one). AS: pages in flight per attention
+// warp (1: one page, cp.async; > 1: the TMA-staged ring, for larger batches).
+template <int BN, int STAGES, int MINB, int MT = BN, int AS = 1>
 __global__ void __launch_bounds__(kThreads, MINB)
     gemm_chain_kernel(const __grid_constant__ ChainMaps maps, const __grid_constant__ ChainArgs args) {
   constexpr int A_BYTES = kBM * kBK * 2;
@@ -692,7 +696,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
   float* rs = red + 4 * BN;                                  // [BN]
   int* slot_s = reinterpret_cast<int*>(rs + BN);             // [64] QKV phases: the tokens' pool slots
   constexpr bool kAttn = MINB == 1;                          // deep (layer) chains carry the attention phase
-  bf16* vs_all = reinterpret_cast<bf16*>((reinterpret_cast<uintptr_t>(slot_s + 64) + 127) & ~uintptr_t(127));
+  uint64_t* abar = reinterpret_cast<uint64_t*>(slot_s + 64);  // [4][AS] attention page barriers (AS > 1)
+  constexpr uintptr_t kVsAlign = AS > 1 ? 1024 : 128;         // TMA 128-byte-swizzle destinations
+  bf16* vs_all = reinterpret_cast<bf16*>((reinterpret_cast<uintptr_t>(abar + 4 * AS) + kVsAlign - 1) &
+                                         ~(kVsAlign - 1));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
@@ -705,6 +712,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
       asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.w[p]) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.x[p]) : "memory");
     }
+    if constexpr (AS > 1)
+      if (args.nattn) asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.pool) : "memory");
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -713,6 +722,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 4);
     }
+    if constexpr (AS > 1)
+      for (int i = 0; i < 4 * AS; ++i) mbar_init(&abar[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
@@ -837,6 +848,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
     if (tr && lane == 0) tr[9] = gtimer();
   } else {
     bool attn0_done = false;
+    uint32_t acnt[4] = {0u, 0u, 0u, 0u};   // attention warps' running page counts (AS > 1)
+    attn::TmaPages tpg;
+    tpg.map = &maps.pool;
+    tpg.block_rows = args.block_rows;
     if constexpr (kAttn) {
       if (args.attn_early && args.nattn && args.attn_before[0] == 0) {
         // The first attention starts before griddepcontrol.wait: its work
@@ -851,10 +866,14 @@ __global__ void __launch_bounds__(kThreads, MINB)
         };
         auto done = [](int, int) { asm volatile("fence.proxy.async;" ::: "memory"); };
         unsigned long long* atr = (tr && ew == 0) ? tr + 16 : nullptr;
-        if (args.attn_kind[0] == 1) attn::attn_cta_phase<128, 4>(aw, cta, G, ew, lane, vs_all, wait_prev, done, atr);
-        else if (args.attn_kind[0] == 2) attn::attn_cta_phase<64, 2>(aw, cta, G, ew, lane, vs_all, wait_prev, done);
-        else if (args.attn_kind[0] == 4) attn::attn_cta_phase<128, 8>(aw, cta, G, ew, lane, vs_all, wait_prev, done);
-        else attn::attn_cta_phase<64, 4>(aw, cta, G, ew, lane, vs_all, wait_prev, done);
+        if (args.attn_kind[0] == 1)
+          attn::attn_cta_phase<128, 4, AS>(aw, cta, G, ew, lane, vs_all, wait_prev, done, atr, &tpg, abar, acnt);
+        else if (args.attn_kind[0] == 2)
+          attn::attn_cta_phase<64, 2, AS>(aw, cta, G, ew, lane, vs_all, wait_prev, done, nullptr, &tpg, abar, acnt);
+        else if (args.attn_kind[0] == 4)
+          attn::attn_cta_phase<128, 8, AS>(aw, cta, G, ew, lane, vs_all, wait_prev, done, nullptr, &tpg, abar, acnt);
+        else
+          attn::attn_cta_phase<64, 4, AS>(aw, cta, G, ew, lane, vs_all, wait_prev, done, nullptr, &tpg, abar, acnt);
         pdl_wait();
         asm volatile("fence.proxy.async;" ::: "memory");
         epi_bar();
@@ -896,10 +915,14 @@ __global__ void __launch_bounds__(kThreads, MINB)
           attn::AttnWork aw = args.at[k];
           aw.tag = ((unsigned)epoch << 4) | (unsigned)(8 + k);
           unsigned long long* atr = (tr && ew == 0 && k == 0) ? tr + 16 : nullptr;
-          if (args.attn_kind[k] == 1) attn::attn_cta_phase<128, 4>(aw, cta, G, ew, lane, vs_all, no_wait, done, atr);
-          else if (args.attn_kind[k] == 2) attn::attn_cta_phase<64, 2>(aw, cta, G, ew, lane, vs_all, no_wait, done);
-          else if (args.attn_kind[k] == 4) attn::attn_cta_phase<128, 8>(aw, cta, G, ew, lane, vs_all, no_wait, done);
-          else attn::attn_cta_phase<64, 4>(aw, cta, G, ew, lane, vs_all, no_wait, done);
+          if (args.attn_kind[k] == 1)
+            attn::attn_cta_phase<128, 4, AS>(aw, cta, G, ew, lane, vs_all, no_wait, done, atr, &tpg, abar, acnt);
+          else if (args.attn_kind[k] == 2)
+            attn::attn_cta_phase<64, 2, AS>(aw, cta, G, ew, lane, vs_all, no_wait, done, nullptr, &tpg, abar, acnt);
+          else if (args.attn_kind[k] == 4)
+            attn::attn_cta_phase<128, 8, AS>(aw, cta, G, ew, lane, vs_all, no_wait, done, nullptr, &tpg, abar, acnt);
+          else
+            attn::attn_cta_phase<64, 4, AS>(aw, cta, G, ew, lane, vs_all, no_wait, done, nullptr, &tpg, abar, acnt);
           asm volatile("fence.proxy.async;" ::: "memory");
           epi_bar();
           if (threadIdx.x == 64) {
@@ -1134,11 +1157,14 @@ constexpr size_t kHeadBytes = kCounterBytes + kPhaseBytes + kAttnWsBytes;   // b
 
 size_t partial_bytes(int M, const SkPlan& p) { return (size_t)p.tiles * p.maxseg * M * kBM * sizeof(unsigned long long); }
 
-template <int BN, bool DEEP = false>
+template <int BN, bool DEEP = false, int AS = 1>
 constexpr size_t sk_extra_bytes() {
-  // DEEP (layer) chains also hold the attention phase's four V pages
+  // DEEP (layer) chains also hold the attention phase's four V pages, or
+  // with AS > 1 four rings of AS (K + V) pages (D = 128 sized, 1 KB aligned)
   return (size_t)BN * kBM * 2 + 5 * BN * sizeof(float) + 64 * sizeof(int) + 64 +
-         (DEEP ? 128 + 4 * (size_t)attn::kAttnWarpBytes : 0);
+         (DEEP ? (AS > 1 ? 1024 + 4 * AS * 8 + 4 * (size_t)AS * attn::tma_page_bytes<128>()
+                         : 128 + 4 * (size_t)attn::kAttnWarpBytes)
+               : 0);
 }
 // Single GEMMs: ~104 KB so two CTAs fit per SM and the next kernel's CTA can
 // become resident and prefetch its weights (PDL) while this one drains.
@@ -1146,34 +1172,53 @@ constexpr size_t sk_extra_bytes() {
 #ifndef ASTRAEA_DEEP_RING_KB
 #define ASTRAEA_DEEP_RING_KB 200   // smem budget of a deep chain's ring + extras (KB)
 #endif
-template <int BN, bool DEEP>
+template <int BN, bool DEEP, int AS = 1>
 constexpr int sk_stages() {
-  return (int)(((DEEP ? ASTRAEA_DEEP_RING_KB : 104) * 1024 - sk_extra_bytes<BN, DEEP>()) / (kBM * kBK * 2 + BN * kBK * 2));
+  return (int)(((DEEP ? ASTRAEA_DEEP_RING_KB : 104) * 1024 - sk_extra_bytes<BN, DEEP, AS>()) /
+               (kBM * kBK * 2 + BN * kBK * 2));
+}
+
+// Attention pages in flight per warp for the batches a BN / MT instantiation
+// serves: small batches keep the one-page walk and the deepest weight ring,
+// batches above 8 trade weight-ring stages for a TMA page ring
+// (ASTRAEA_CHAIN_ATTN_STAGES at build time).
+#ifndef ASTRAEA_CHAIN_ATTN_STAGES
+#define ASTRAEA_CHAIN_ATTN_STAGES 3
+#endif
+template <int BN, int MT>
+constexpr int chain_attn_stages() {
+  return (BN == 16 && MT <= 8) ? 1 : ASTRAEA_CHAIN_ATTN_STAGES;
+}
+
+template <int BN, bool DEEP, int MT>
+int launch_chain_mt(const ChainMaps& maps, const ChainArgs& a, cudaStream_t st, int which) {
+  constexpr int AS = DEEP ? chain_attn_stages<BN, MT>() : 1;
+  constexpr int S = sk_stages<BN, DEEP, AS>();
+  constexpr int MB = DEEP ? 1 : 2;
+  auto kern = gemm_chain_kernel<BN, S, MB, MT, AS>;
+  constexpr size_t smem = 1024 + (size_t)S * (kBM * kBK * 2 + BN * kBK * 2) + (2 * S + 4) * 8 + 16 +
+                          sk_extra_bytes<BN, DEEP, AS>();
+  static bool attr = false;
+  if (!attr) {
+    ASTRAEA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  (void)which;
+  ASTRAEA_TRY(launch_k(kern, dim3(a.grid), dim3(kThreads), smem, st, maps, a));
+  return 0;
 }
 
 template <int BN, bool DEEP>
 int launch_chain(const ChainMaps& maps, const ChainArgs& a, cudaStream_t st) {
-  constexpr int S = sk_stages<BN, DEEP>();
-  constexpr int MB = DEEP ? 1 : 2;
   // token-loop bound: the next power of two >= M (its own instantiation, so
   // the per-phase epilogue code a small batch executes stays small)
-  int which = 0;
-  auto kern = gemm_chain_kernel<BN, S, MB>;
   if constexpr (BN == 16) {
-    if (a.M <= 1) kern = gemm_chain_kernel<BN, S, MB, 1>, which = 1;
-    else if (a.M <= 2) kern = gemm_chain_kernel<BN, S, MB, 2>, which = 2;
-    else if (a.M <= 4) kern = gemm_chain_kernel<BN, S, MB, 4>, which = 3;
-    else if (a.M <= 8) kern = gemm_chain_kernel<BN, S, MB, 8>, which = 4;
+    if (a.M <= 1) return launch_chain_mt<BN, DEEP, 1>(maps, a, st, 1);
+    if (a.M <= 2) return launch_chain_mt<BN, DEEP, 2>(maps, a, st, 2);
+    if (a.M <= 4) return launch_chain_mt<BN, DEEP, 4>(maps, a, st, 3);
+    if (a.M <= 8) return launch_chain_mt<BN, DEEP, 8>(maps, a, st, 4);
   }
-  constexpr size_t smem = 1024 + (size_t)S * (kBM * kBK * 2 + BN * kBK * 2) + (2 * S + 4) * 8 + 16 +
-                          sk_extra_bytes<BN, DEEP>();
-  static bool attr[5] = {false, false, false, false, false};
-  if (!attr[which]) {
-    ASTRAEA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr[which] = true;
-  }
-  ASTRAEA_TRY(launch_k(kern, dim3(a.grid), dim3(kThreads), smem, st, maps, a));
-  return 0;
+  return launch_chain_mt<BN, DEEP, BN>(maps, a, st, 0);
 }
 
 int to_epi(const astraea_epilogue* in, int N, Epi* e) {
@@ -1424,6 +1469,21 @@ static int run_chain(int M, int nph, const astraea_gemm_phase* ph, void* ws, siz
     a.pf_layer = (pf && at->layer + 1 < g.num_layers) ? at->layer + 1 : -1;
   }
   a.nattn = nattn;
+  a.block_rows = 0;
+  if (nattn > 0) {
+    // the TMA-staged attention instantiations (AS > 1) read pages through
+    // this map; every attention of a launch uses the same pool
+    const astraea_kv_geometry& g = ats[0].geo;
+    for (int k = 1; k < nattn; ++k)
+      if (ats[k].pool_dev != ats[0].pool_dev || ats[k].geo.num_blocks != g.num_blocks ||
+          ats[k].geo.head_dim != g.head_dim || ats[k].geo.num_kv_heads != g.num_kv_heads ||
+          ats[k].geo.num_layers != g.num_layers)
+        return ASTRAEA_EINVAL;
+    a.block_rows = g.num_layers * 2 * g.num_kv_heads * g.block_tokens;
+    const int rc = make_map(&maps.pool, ats[0].pool_dev, (long long)g.num_blocks * a.block_rows, g.head_dim,
+                            g.head_dim, g.block_tokens);
+    if (rc) return rc;
+  }
   static const int attn_early = [] {
     const char* e = getenv("ASTRAEA_CHAIN_ATTN_EARLY");
     return e ? atoi(e) : 1;

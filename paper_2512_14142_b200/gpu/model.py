@@ -238,6 +238,10 @@ class LlamaRunner:
         # the layer's decode attention runs inside its chained-GEMM launch
         # (astraea_gemm_chain_attn) instead of as a separate kernel
         self.fuse_attention = True
+        # above this batch the layer's attention runs as its own TMA-staged
+        # kernel before the chain (more pages in flight than the chain's
+        # epilogue warps can keep; tools/attn_ab.py)
+        self.fuse_max_batch = 64
         self.l2_ahead = 0
         self._mk = None
         self._programs: dict = {}
@@ -362,7 +366,7 @@ class LlamaRunner:
                         positions=positions, slots=slots, rope_theta=cfg.rope_theta, rope_table=cs)
 
         ops.gemm_ex(**qkv(0, ssq0), workspace=ws, stream=stream)
-        fuse = self.fuse_attention and self._attn_fusable()
+        fuse = self.fuse_attention and self._attn_fusable() and B <= self.fuse_max_batch
         per = self.chain_layers if fuse else 1
         for l0 in range(0, cfg.num_layers, per):
             phases, attns = [], []
