@@ -351,6 +351,11 @@ ASTRAEA_API int astraea_step_launch(int32_t M, int32_t nphases, const void* prog
  * Pass NULL to disable. */
 ASTRAEA_API int astraea_debug_gemm_trace(void* buf, int32_t slots, int32_t slot_stride);
 
+/* Diagnostics: when buf != NULL, each following tcgen05 prefill-attention
+ * launch writes per-CTA %globaltimer stamps [grid][16] into buf (see
+ * prefill_tc.cu); NULL disables. */
+ASTRAEA_API int astraea_debug_prefill_trace(void* buf);
+
 /* RoPE angle table for a batch: table[t][i] = (cos, sin)(positions[t] * theta^(-2i/D)),
  * i < D/2 -- computed once per forward and shared by every layer's QKV epilogue. */
 ASTRAEA_API int astraea_rope_table(const int32_t* positions_dev, int32_t T, int32_t head_dim, float rope_theta,

@@ -24,6 +24,13 @@
 
 using namespace astraea;
 
+namespace astraea {
+// K7 on tcgen05 (prefill_tc.cu)
+int prefill_tc_launch(const astraea_kv_geometry* g, const void* pool, int32_t layer, const void* q, int32_t q_stride,
+                      const int32_t* cu_q, int32_t S, int32_t max_q_len, int32_t Hq, const int32_t* table,
+                      int32_t max_blocks, const int32_t* ctx, float scale, void* out, cudaStream_t st);
+}
+
 namespace {
 
 constexpr int kBT = 16;         // tokens per block
@@ -886,6 +893,15 @@ extern "C" int astraea_paged_prefill_attention(const astraea_kv_geometry* g, con
     return ASTRAEA_EINVAL;
   if (S == 0 || max_q_len == 0) return ASTRAEA_OK;
   if (Hq % g->num_kv_heads || q_stride < Hq * g->head_dim) return ASTRAEA_EINVAL;
+  static const bool use_tc = [] {
+    const char* e = getenv("ASTRAEA_PREFILL_ATTN");
+    return !(e && e[0] == 'm');   // "m": the mma.sync kernel below
+  }();
+  if (use_tc) {
+    const int rc = astraea::prefill_tc_launch(g, pool, layer, q, q_stride, cu_q, S, max_q_len, Hq, table, max_blocks,
+                                              ctx, scale, out, (cudaStream_t)stream);
+    if (rc != ASTRAEA_EUNSUPPORTED) return rc;
+  }
   PrefillParams p;
   p.pool = (const bf16*)pool;
   p.q = (const bf16*)q;

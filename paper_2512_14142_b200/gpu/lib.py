@@ -159,6 +159,7 @@ SIGNATURES = {
     "astraea_gemm_bf16_ex": (
         ctypes.c_int, [_vp, _i32, _vp, _i32, _vp, _i32, _i32, _i32, _i32, ctypes.POINTER(Epilogue), _vp, _sz, _vp]),
     "astraea_debug_gemm_trace": (ctypes.c_int, [_vp, _i32, _i32]),
+    "astraea_debug_prefill_trace": (ctypes.c_int, [_vp]),
     "astraea_rope_table": (ctypes.c_int, [_vp, _i32, _i32, _f32, _vp, _vp]),
     "astraea_gemm_chain_workspace_bytes": (_sz, [_i32, _i32, ctypes.POINTER(GemmPhase)]),
     "astraea_gemm_chain": (ctypes.c_int, [_i32, _i32, ctypes.POINTER(GemmPhase), _vp, _sz, _vp]),

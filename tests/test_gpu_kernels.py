@@ -169,9 +169,14 @@ def test_decode_attention(Hq, Hkv, D, ctxs):
 
 # ---------------------------------------------------------------- K7 prefill attention
 
-@pytest.mark.parametrize("Hq,Hkv,D", [(32, 8, 128), (8, 2, 64)])
-@pytest.mark.parametrize("lens_ctx", [[(5, 5)], [(64, 64), (1, 300), (130, 1100)], [(700, 2316)]])
+@pytest.mark.parametrize("Hq,Hkv,D", [(32, 8, 128), (8, 2, 64), (8, 1, 128), (4, 2, 64)])
+@pytest.mark.parametrize("lens_ctx", [[(5, 5)], [(64, 64), (1, 300), (130, 1100)], [(700, 2316)],
+                                      [(33, 1000), (17, 17), (100, 2000)], [(2048, 2048)]])
 def test_prefill_attention(Hq, Hkv, D, lens_ctx):
+    """Varlen paged prefill (tcgen05 kernel; G = 1..8 q heads per kv head as
+    the 128 MMA rows) vs the fp32 oracle: fresh prompts, short appends onto
+    long resident contexts, a 2048-token causal prompt (16 KV tiles, the
+    lazy-rescale path), tiles that end mid-page."""
     Lyr = 2
     S = len(lens_ctx)
     max_blocks = max((c + 15) // 16 for _, c in lens_ctx)
