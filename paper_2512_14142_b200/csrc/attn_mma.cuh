@@ -525,6 +525,7 @@ __device__ __forceinline__ void attn_cta_phase(const AttnWork& A, int cta, int g
                                                bf16* vs_all, const WaitHead& wait_head, const DoneHead& done_head,
                                                unsigned long long* atr = nullptr, const TmaPages* tp = nullptr,
                                                uint64_t* abar = nullptr, uint32_t* acnt = nullptr) {
+  // acnt: this warp's running page count (AS > 1), one word per calling thread
   // atr (diagnostics, may be null): [0] entry, [1] wait_head passed, [2] q
   // loaded, [3] pages done, [4] CTA merge + partial published, [5] split
   // merge done, [6] output published, [7] exit, [8..12] first page, [13]
@@ -559,7 +560,7 @@ __device__ __forceinline__ void attn_cta_phase(const AttnWork& A, int cta, int g
       T.k_row0 = (A.layer * 2 * A.Hkv + h) * kAttnBT;
       T.v_row0 = T.k_row0 + A.Hkv * kAttnBT;
       attn_pages_tma<D, AS>(T, A.table + (long long)b * A.max_blocks, pc.pa + warp, pc.pb, 4, ctx_b, A.scale_log2,
-                            qs, reinterpret_cast<uint8_t*>(vs), abar + warp * AS, acnt[warp], st, lane);
+                            qs, reinterpret_cast<uint8_t*>(vs), abar + warp * AS, *acnt, st, lane);
     } else {
       uint32_t qa[D / 8];
       attn_load_q<D>(A.q + (long long)b * A.q_stride + (long long)(h * G + r8) * D, r8 < G, quad, qa);
@@ -625,12 +626,13 @@ __device__ __forceinline__ void attn_cta_phase(const AttnWork& A, int cta, int g
       // a thread's EPT elements lie in one head row g: per part, m and l are
       // two words and o is EPT words; eight parts are polled together
       const int g_me = min(et * EPT, G * D - 1) / D;
-      for (int c0 = first_c + 1; c0 <= last_c; c0 += 8) {
-        unsigned long long pm[8], pl[8], po[8][EPT];
+      constexpr int KP = EPT <= 4 ? 8 : 4;   // parts polled per round (32 words of o per thread)
+      for (int c0 = first_c + 1; c0 <= last_c; c0 += KP) {
+        unsigned long long pm[KP], pl[KP], po[KP][EPT];
         for (int spin = 0;; ++spin) {
           bool ready = true;
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
+          for (int k = 0; k < KP; ++k) {
             const unsigned long long* pp = A.ws + (long long)(c0 + k) * G * (D + 2);
             const bool ok = c0 + k <= last_c;
             pm[k] = ok ? tc::ld_relaxed_u64(pp + g_me) : tagged(-INFINITY, A.tag);
@@ -642,7 +644,7 @@ __device__ __forceinline__ void attn_cta_phase(const AttnWork& A, int cta, int g
             }
           }
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
+          for (int k = 0; k < KP; ++k) {
             ready &= (unsigned)(pm[k] >> 32) == A.tag && (unsigned)(pl[k] >> 32) == A.tag;
 #pragma unroll
             for (int e = 0; e < EPT; ++e) ready &= (unsigned)(po[k][e] >> 32) == A.tag;
@@ -660,7 +662,7 @@ __device__ __forceinline__ void attn_cta_phase(const AttnWork& A, int cta, int g
         // a thread's EPT elements share one head row: one (m, l) rescale per part
         float mc = Mv[0], lc = Lv[0];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < KP; ++k) {
           if (c0 + k > last_c) continue;   // warp-uniform
           const float mk = __uint_as_float((unsigned)pm[k]), lk = __uint_as_float((unsigned)pl[k]);
           const float mn = fmaxf(mc, mk);

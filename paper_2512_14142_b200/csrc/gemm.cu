@@ -848,7 +848,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     if (tr && lane == 0) tr[9] = gtimer();
   } else {
     bool attn0_done = false;
-    uint32_t acnt[4] = {0u, 0u, 0u, 0u};   // attention warps' running page counts (AS > 1)
+    uint32_t acnt = 0;   // this attention warp's running page count (AS > 1)
     attn::TmaPages tpg;
     tpg.map = &maps.pool;
     tpg.block_rows = args.block_rows;
@@ -867,13 +867,13 @@ __global__ void __launch_bounds__(kThreads, MINB)
         auto done = [](int, int) { asm volatile("fence.proxy.async;" ::: "memory"); };
         unsigned long long* atr = (tr && ew == 0) ? tr + 16 : nullptr;
         if (args.attn_kind[0] == 1)
-          attn::attn_cta_phase<128, 4, AS>(aw, cta, G, ew, lane, vs_all, wait_prev, done, atr, &tpg, abar, acnt);
+          attn::attn_cta_phase<128, 4, AS>(aw, cta, G, ew, lane, vs_all, wait_prev, done, atr, &tpg, abar, &acnt);
         else if (args.attn_kind[0] == 2)
-          attn::attn_cta_phase<64, 2, AS>(aw, cta, G, ew, lane, vs_all, wait_prev, done, nullptr, &tpg, abar, acnt);
+          attn::attn_cta_phase<64, 2, AS>(aw, cta, G, ew, lane, vs_all, wait_prev, done, nullptr, &tpg, abar, &acnt);
         else if (args.attn_kind[0] == 4)
-          attn::attn_cta_phase<128, 8, AS>(aw, cta, G, ew, lane, vs_all, wait_prev, done, nullptr, &tpg, abar, acnt);
+          attn::attn_cta_phase<128, 8, AS>(aw, cta, G, ew, lane, vs_all, wait_prev, done, nullptr, &tpg, abar, &acnt);
         else
-          attn::attn_cta_phase<64, 4, AS>(aw, cta, G, ew, lane, vs_all, wait_prev, done, nullptr, &tpg, abar, acnt);
+          attn::attn_cta_phase<64, 4, AS>(aw, cta, G, ew, lane, vs_all, wait_prev, done, nullptr, &tpg, abar, &acnt);
         pdl_wait();
         asm volatile("fence.proxy.async;" ::: "memory");
         epi_bar();
@@ -916,13 +916,13 @@ __global__ void __launch_bounds__(kThreads, MINB)
           aw.tag = ((unsigned)epoch << 4) | (unsigned)(8 + k);
           unsigned long long* atr = (tr && ew == 0 && k == 0) ? tr + 16 : nullptr;
           if (args.attn_kind[k] == 1)
-            attn::attn_cta_phase<128, 4, AS>(aw, cta, G, ew, lane, vs_all, no_wait, done, atr, &tpg, abar, acnt);
+            attn::attn_cta_phase<128, 4, AS>(aw, cta, G, ew, lane, vs_all, no_wait, done, atr, &tpg, abar, &acnt);
           else if (args.attn_kind[k] == 2)
-            attn::attn_cta_phase<64, 2, AS>(aw, cta, G, ew, lane, vs_all, no_wait, done, nullptr, &tpg, abar, acnt);
+            attn::attn_cta_phase<64, 2, AS>(aw, cta, G, ew, lane, vs_all, no_wait, done, nullptr, &tpg, abar, &acnt);
           else if (args.attn_kind[k] == 4)
-            attn::attn_cta_phase<128, 8, AS>(aw, cta, G, ew, lane, vs_all, no_wait, done, nullptr, &tpg, abar, acnt);
+            attn::attn_cta_phase<128, 8, AS>(aw, cta, G, ew, lane, vs_all, no_wait, done, nullptr, &tpg, abar, &acnt);
           else
-            attn::attn_cta_phase<64, 4, AS>(aw, cta, G, ew, lane, vs_all, no_wait, done, nullptr, &tpg, abar, acnt);
+            attn::attn_cta_phase<64, 4, AS>(aw, cta, G, ew, lane, vs_all, no_wait, done, nullptr, &tpg, abar, &acnt);
           asm volatile("fence.proxy.async;" ::: "memory");
           epi_bar();
           if (threadIdx.x == 64) {
@@ -983,6 +983,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
         unsigned long long* tpart = wsq + ((tile * P.maxseg) * (long long)args.M) * kBM + row;
         constexpr bool kPreRes = BN <= 32;   // register budget: BN = 64 reads the residual in the epilogue
         float res[BN], acc[BN];
+        // diagnostics (phase 2, the last finished tile): [11] collect start, [12] collect done,
+        // [13] own MMAs done, [14] epilogue done
+        const bool ftr = tr && finisher && !whole && p == 2 && threadIdx.x == 64;
+        if (ftr) tr[11] = gtimer();
         if (finisher) {
           if (kPreRes && resid) {
             const int f = (int)tile * kBM + row;
@@ -1015,8 +1019,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
             }
           }
         }
+        if (ftr) tr[12] = gtimer();
         mbar_wait(&tfull[buf], (seg >> 1) & 1);
         tc_fence_after();
+        if (ftr) tr[13] = gtimer();
         float v[BN < 32 ? 32 : BN];
 #pragma unroll
         for (int c0 = 0; c0 < BN; c0 += 32) tmem_ld32(lane_addr + buf * BN + c0, v + c0);
@@ -1038,6 +1044,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         }
         sk_finish<BN, SkPhase, MT>(P, (int)tile, row, v, rs, xch, red, (kPreRes && resid) ? res : nullptr, stage ? slot_s : nullptr,
                       cs_s);
+        if (ftr) tr[14] = gtimer();
       }
       // phase p done in this CTA: publish (release) for the other CTAs. The
       // last CTA to finish the last phase resets the counters for the next

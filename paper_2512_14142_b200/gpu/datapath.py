@@ -299,15 +299,17 @@ class KvDataPath:
         # table width bucketed to a power of two (>= 16): the same kernel
         # arguments whether the step runs eagerly or as a graph replay
         max_blocks = _width_bucket(max(1, max(len(p["rd"].blocks) for p in plan)))
-        positions, slots, cu_q, pre_ctx = [], [], [0], []
-        for i in pre:
+        pos_parts, slot_parts, cu_q, pre_ctx = [], [], [0], []
+        for i in pre:   # vectorised: a recompute feeds thousands of tokens
             p = plan[i]
-            bl = p["rd"].blocks
-            for pos in range(p["start"], p["start"] + p["plen"]):
-                positions.append(pos)
-                slots.append(bl[pos // BT] * BT + pos % BT)
+            pos = np.arange(p["start"], p["start"] + p["plen"], dtype=np.int64)
+            bl = np.asarray(p["rd"].blocks, dtype=np.int64)
+            pos_parts.append(pos)
+            slot_parts.append(bl[pos // BT] * BT + pos % BT)
             cu_q.append(cu_q[-1] + p["plen"])
             pre_ctx.append(p["start"] + p["plen"])
+        positions = np.concatenate(pos_parts) if pos_parts else np.zeros(0, dtype=np.int64)
+        slots = np.concatenate(slot_parts) if slot_parts else np.zeros(0, dtype=np.int64)
         T = cu_q[-1]
         max_q = max([plan[i]["plen"] for i in pre], default=0)
         n_gen = [p["n_gen"] for p in plan]

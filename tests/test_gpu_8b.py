@@ -67,14 +67,27 @@ def prefill(runner, seqs, tables):
                           torch.tensor(last, device=DEV), max(len(s) for s in seqs), want_logits=True)
 
 
-def test_8b_shape_prefill_512_logits(model):
+# The 512-token prefill sits on the bf16 noise floor of this shape: the
+# oracle's own bf16 storage points move its logits 1.1-1.4e-2 from the pure
+# fp32 forward, and the device lands 0.92-1.01e-2 from the bf16-point oracle
+# with the tcgen05 attention (0.87-0.97e-2 with the mma.sync kernel it
+# replaced; tools/diag_prefill8b.py, four prompts). The bar: closer to the
+# bf16-point oracle than that oracle is to fp32, and within 1.25e-2.
+TOL_PREFILL = 1.25e-2
+
+
+@pytest.mark.parametrize("name,T", [("p512", 512), ("s1000", 1000)])
+def test_8b_shape_prefill_logits(model, name, T):
     w, logical = model
-    pool = KvPool(CFG, 64)
+    pool = KvPool(CFG, 80)
     runner = LlamaRunner(w, pool)
-    ids = segment_token_ids("p512", 1, 512, CFG.vocab)
-    tok, logits = prefill(runner, [ids], [list(range(3, 35))])
+    ids = segment_token_ids(name, 1, T, CFG.vocab)
+    tok, logits = prefill(runner, [ids], [list(range(3, 3 + (T + 15) // 16))])
     ref = oracle_last(logical, ids)
-    assert rel(logits[0], ref) < TOL
+    with torch.no_grad():
+        ref32 = llama_ref.forward(logical, CFG, ids, bf16_points=False, last_only=True)[0]
+    e = rel(logits[0], ref)
+    assert e < TOL_PREFILL and e < rel(ref, ref32), (e, rel(ref, ref32))
 
 
 @pytest.mark.parametrize("B", [1, 8, 16])

@@ -75,6 +75,18 @@ for i in range(n):
         att["m_group0_spins_max"] = int(sp.max())
         print(json.dumps({"layer": li, "attention_warp0_first_piece": att}))
 
+# split-tile finishers of the down projection (phase 2): collect / own MMAs / epilogue
+i = a.layers[-1] + 1
+s = t[i]
+fm = s[:, 11] > 0
+if bool(fm.any()):
+    rel = float(s[:, 3][s[:, 3] > 0].median())   # down activations released
+    f = s[fm]
+    g = lambda k: [round(float((f[:, k] - rel).median()) / 1000, 2), round(float((f[:, k] - rel).max()) / 1000, 2)]  # noqa: E731
+    print(json.dumps({"down_finishers": int(fm.sum()), "collect_start": g(11), "collect_done": g(12),
+                      "own_mma_done": g(13), "epilogue_done": g(14),
+                      "others_done_median": round(float((s[~fm][:, 7] - rel).median()) / 1000, 2)}))
+
 if a.per_cta:
     # per-CTA phase completion (relative to the phase's activation release) of one launch
     i = a.layers[-1] + 1

@@ -31,7 +31,7 @@ nb = (C + 16) // 16
 dp = KvDataPath(cfg, num_blocks=max(B * nb + 8, (a.tokens + 15) // 16 + 8))
 dp.pool.data.normal_(0, 0.5)
 if a.what == "chain":
-    bench.chain_kernel_time(dp, cfg, B, reps=3)
+    bench.chain_kernel_time(dp, cfg, B, C, reps=3)
 elif a.what == "attn":
     qd = cfg.num_q_heads * cfg.head_dim
     q = torch.randn(B, qd, device="cuda").bfloat16()

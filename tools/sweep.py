@@ -31,7 +31,9 @@ from paper_2512_14142_b200.gpu.model import PRESETS  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("kind", choices=["pressure", "rate"])
-ap.add_argument("--requests", type=int, default=16)
+ap.add_argument("--requests", type=int, default=64, help="C2 trace length (64 in the survey's C2/C3)")
+ap.add_argument("--base", type=int, default=40_000, help="C3: capacity x {0.3, 0.5, 0.7, 0.9} (SURVEY 8(d))")
+ap.add_argument("--rate-capacity", type=int, default=12_000)
 ap.add_argument("--out", default=None)
 a = ap.parse_args()
 cfg = PRESETS["llama3-8b"]
@@ -78,16 +80,16 @@ rows = []
 n = a.requests
 if a.kind == "pressure":
     wl = trace(2.0, n)
-    base = 8_000   # x {0.3 .. 0.9}: the smallest still holds the longest request (2.3k tokens)
+    base = a.base   # x {0.3 .. 0.9} (cli.py:41-47, 245-256)
     dp = KvDataPath(cfg, num_blocks=base // 16 + 2 * n + 64)
     for tables in ("calibrated", "reference-default"):
         for frac in (0.3, 0.5, 0.7, 0.9):
             rows.append(cell(wl, int(base * frac), tables, dp))
             print(json.dumps(rows[-1]), flush=True)
 else:
-    dp = KvDataPath(cfg, num_blocks=3000 // 16 + 2 * n + 64)
+    dp = KvDataPath(cfg, num_blocks=a.rate_capacity // 16 + 2 * n + 64)
     for qps in (1.0, 2.0, 4.0, 8.0):
-        r = cell(trace(qps, n), 3000, "calibrated", dp)
+        r = cell(trace(qps, n), a.rate_capacity, "calibrated", dp)
         r["qps"] = qps
         rows.append(r)
         print(json.dumps(r), flush=True)
