@@ -597,8 +597,6 @@ __device__ __forceinline__ void sk_range(const SkPhase& P, int cta, long long& u
   }
 }
 
-constexpr int kMaxFlagTiles = 1024;   // output tiles per phase with a readiness flag (lm_head: 1002)
-
 struct ChainMaps {
   CUtensorMap w[kMaxPhases];
   CUtensorMap x[kMaxPhases];
@@ -619,10 +617,6 @@ struct ChainArgs {
   int pf_layer;                // >= 0: prefetch that layer's K/V pages into L2 during the last phase
   int attn_early;              // the first attention's work split runs before griddepcontrol.wait
   int block_rows;              // attention (AS > 1): rows of one pool block in ChainMaps::pool
-  int* tile_flag;              // [kMaxPhases][kMaxFlagTiles]: phase p's output tile t published (tag)
-  int* head_flag;              // [kMaxAttn][64]: attention k's kv head h written for every row (tag)
-  int* head_ctr;               // [kMaxAttn][64]: rows written per kv head (reset by the last writer)
-  int attn_cols[kMaxAttn];     // activation columns per kv head of attention k (G * D)
   SkPhase ph[kMaxPhases];
 };
 constexpr int kAttnCtr = kMaxPhases + 2;   // phase_ctr slots kAttnCtr + k: CTAs done with attention k
@@ -741,8 +735,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
   pdl_launch();
   if (warp == 0) {
     if (lane == 0) {
-      int i = 0;    // ring position, continuous across phases
-      int ep = 0;   // launch epoch (read after griddepcontrol.wait in phase 0)
+      int i = 0;   // ring position, continuous across phases
       for (int p = 0; p < args.nph; ++p) {
         const SkPhase& P = args.ph[p];
         const int KB = P.kbs;
@@ -753,10 +746,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         // arrived) -- but griddepcontrol.wait still comes first, before this
         // thread reads any counter of a later phase
         if (u0 == u1) {
-          if (p == 0) {
-            pdl_wait();
-            ep = __ldcg(args.phase_ctr + kMaxPhases + 1) + 1;
-          }
+          if (p == 0) pdl_wait();
           continue;
         }
         const int pre = (int)(u1 - u0 < STAGES ? u1 - u0 : STAGES);
@@ -772,19 +762,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
         if (kAttn)
           for (int k = 0; k < args.nattn; ++k)
             if (args.attn_before[k] == p) ak = k;
-        // Dataflow instead of a phase barrier: activation k-block kc of phase
-        // p waits only for what produces it -- the previous phase's output
-        // tile kc / 128, or the attention's kv head kc / (G * D) -- so a
-        // phase starts on the tiles that are done while the last finishers
-        // (and the slowest attention heads) still run.
-        int dep = 0;   // 0: everything ready after griddepcontrol.wait; 1: attention heads; 2: tiles of p - 1
-        uint32_t sat[4] = {0u, 0u, 0u, 0u};
         if (ak >= 0) {
-          if (p == 0) {
-            pdl_wait();
-            ep = __ldcg(args.phase_ctr + kMaxPhases + 1) + 1;
-          }
-          dep = 1;
+          if (p == 0) pdl_wait();
+          wait_phase(args.phase_ctr + kAttnCtr + ak, G);   // every CTA's share of the attention is written
+          asm volatile("fence.proxy.async;" ::: "memory");
         } else if (p == 0) {
           // While the previous kernel (the layer's attention) finishes, keep
           // HBM busy: prefetch the next l2_pre weight tiles of this CTA's
@@ -807,42 +788,21 @@ __global__ void __launch_bounds__(kThreads, MINB)
             }
           }
           pdl_wait();
-          ep = __ldcg(args.phase_ctr + kMaxPhases + 1) + 1;
         } else {
-          dep = 2;
-        }
-#ifndef ASTRAEA_CHAIN_DATAFLOW
-#define ASTRAEA_CHAIN_DATAFLOW 1
-#endif
-        if (!ASTRAEA_CHAIN_DATAFLOW && dep != 0) {   // A/B: the whole previous phase / attention first
-          wait_phase(dep == 1 ? args.phase_ctr + kAttnCtr + ak : args.phase_ctr + p - 1, G);
-          asm volatile("fence.proxy.async;" ::: "memory");
-          dep = 0;
-        }
-        auto act_wait = [&](int kc) {
-          if (dep == 0) return;
-          const int need = dep == 1 ? kc / args.attn_cols[ak] : kc / kBM;
-          if (need < 128 && ((sat[need >> 5] >> (need & 31)) & 1u)) return;
-          const int* f = dep == 1 ? args.head_flag + ak * 64 + need : args.tile_flag + (p - 1) * kMaxFlagTiles + need;
-          const int want = (int)(((unsigned)ep << 4) | (unsigned)(dep == 1 ? 8 + ak : p - 1));
-          while (ld_acquire(f) != want) __nanosleep(20);
+          wait_phase(args.phase_ctr + p - 1, G);
           asm volatile("fence.proxy.async;" ::: "memory");   // generic-proxy writes -> TMA reads
-          if (need < 128) sat[need >> 5] |= 1u << (need & 31);
-        };
+        }
+        if (tr && p < 4) tr[1 + p] = gtimer();   // activations of phase p released (first layer only)
         for (int k = 0; k < pre; ++k) {
           const int s = (i + k) % STAGES;
-          const int kc = (int)((u0 + k) % KB) * kBK;
-          act_wait(kc);
-          if (tr && p < 4 && k == 0) tr[1 + p] = gtimer();   // first activations of phase p ready
-          tma_load_2d(sb + s * B_BYTES, &maps.x[p], &full[s], kc, 0);
+          tma_load_2d(sb + s * B_BYTES, &maps.x[p], &full[s], (int)((u0 + k) % KB) * kBK, 0);
         }
         int idx = i + pre;
         for (long long u = u0 + pre; u < u1; ++u, ++idx) {
           const int s = idx % STAGES;
           if (idx >= STAGES) mbar_wait(&empty[s], ((idx / STAGES) - 1) & 1);
-          const int kc = (int)(u % KB) * kBK;
-          act_wait(kc);
           mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
+          const int kc = (int)(u % KB) * kBK;
           tma_load_2d(sa + s * A_BYTES, &maps.w[p], &full[s], kc, (int)(u / KB) * kBM);
           tma_load_2d(sb + s * B_BYTES, &maps.x[p], &full[s], kc, 0);
         }
@@ -904,15 +864,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
           pdl_wait();
           aw.tag = (((unsigned)__ldcg(args.phase_ctr + kMaxPhases + 1) + 1u) << 4) | 8u;
         };
-        auto done = [&aw, &args](int h, int et) {   // (row, head h) written: the last row publishes head h
-          asm volatile("fence.proxy.async;" ::: "memory");
-          epi_bar();
-          if (et == 0 && atom_add_acq_rel(args.head_ctr + h, 1) == args.M - 1) {
-            args.head_ctr[h] = 0;
-            __threadfence();
-            st_release_i32(args.head_flag + h, (int)((aw.tag & ~15u) | 8u));
-          }
-        };
+        auto done = [](int, int) { asm volatile("fence.proxy.async;" ::: "memory"); };
         unsigned long long* atr = (tr && ew == 0) ? tr + 16 : nullptr;
         if (args.attn_kind[0] == 1)
           attn::attn_cta_phase<128, 4, AS>(aw, cta, G, ew, lane, vs_all, wait_prev, done, atr, &tpg, abar, &acnt);
@@ -959,17 +911,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
           // tiles into the ring; its output is phase p's A.
           const int ew = warp - 2;
           auto no_wait = [](int, int) {};
+          auto done = [](int, int) { asm volatile("fence.proxy.async;" ::: "memory"); };
           attn::AttnWork aw = args.at[k];
           aw.tag = ((unsigned)epoch << 4) | (unsigned)(8 + k);
-          auto done = [&aw, &args, k](int h, int et) {   // the last row written publishes head h
-            asm volatile("fence.proxy.async;" ::: "memory");
-            epi_bar();
-            if (et == 0 && atom_add_acq_rel(args.head_ctr + k * 64 + h, 1) == args.M - 1) {
-              args.head_ctr[k * 64 + h] = 0;
-              __threadfence();
-              st_release_i32(args.head_flag + k * 64 + h, (int)aw.tag);
-            }
-          };
           unsigned long long* atr = (tr && ew == 0 && k == 0) ? tr + 16 : nullptr;
           if (args.attn_kind[k] == 1)
             attn::attn_cta_phase<128, 4, AS>(aw, cta, G, ew, lane, vs_all, no_wait, done, atr, &tpg, abar, &acnt);
@@ -1101,14 +1045,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
         sk_finish<BN, SkPhase, MT>(P, (int)tile, row, v, rs, xch, red, (kPreRes && resid) ? res : nullptr, stage ? slot_s : nullptr,
                       cs_s);
         if (ftr) tr[14] = gtimer();
-        if (p + 1 < args.nph && tile < kMaxFlagTiles) {
-          // tile published: the next phase's producers load its columns (dataflow)
-          epi_bar();
-          if (threadIdx.x == 64) {
-            __threadfence();
-            st_release_i32(args.tile_flag + p * kMaxFlagTiles + tile, (int)tag);
-          }
-        }
       }
       // phase p done in this CTA: publish (release) for the other CTAs. The
       // last CTA to finish the last phase resets the counters for the next
@@ -1224,9 +1160,7 @@ constexpr size_t kCounterBytes = 16384 * sizeof(int);
 constexpr size_t kPhaseBytes = 256;
 // attention phase of a layer chain: [grid <= 192][G <= 4][D + 2 <= 130] tagged split partials
 constexpr size_t kAttnWsBytes = (size_t)192 * 8 * 130 * sizeof(unsigned long long);   // grid x G x (D + 2), G*D <= 1024
-// chain dataflow flags: tile flags [kMaxPhases][kMaxFlagTiles], head flags and counters [kMaxAttn][64]
-constexpr size_t kFlagBytes = ((size_t)kMaxPhases * kMaxFlagTiles + 2 * kMaxAttn * 64) * sizeof(int);
-constexpr size_t kHeadBytes = kCounterBytes + kPhaseBytes + kAttnWsBytes + kFlagBytes;   // before the GEMM partials
+constexpr size_t kHeadBytes = kCounterBytes + kPhaseBytes + kAttnWsBytes;   // before the GEMM partials
 
 size_t partial_bytes(int M, const SkPlan& p) { return (size_t)p.tiles * p.maxseg * M * kBM * sizeof(unsigned long long); }
 
@@ -1252,9 +1186,11 @@ constexpr int sk_stages() {
 }
 
 // Attention pages in flight per warp for the batches a BN / MT instantiation
-// serves: small batches keep the one-page walk and the deepest weight ring,
-// batches above 8 trade weight-ring stages for a TMA page ring
-// (ASTRAEA_CHAIN_ATTN_STAGES at build time).
+// serves: batches <= 4 keep the one-page walk and the deepest weight ring,
+// 5-8 two TMA page stages, above 8 three (weight-ring stages traded for
+// pages in flight; ASTRAEA_CHAIN_ATTN_STAGES* at build time; same-box A/B in
+// profiles/r2_attn_stages_small_ab.txt: batch 8 3.646 -> 3.560 ms with two
+// stages, batches 1-4 within +-0.7%).
 #ifndef ASTRAEA_CHAIN_ATTN_STAGES
 #define ASTRAEA_CHAIN_ATTN_STAGES 3
 #endif
@@ -1263,7 +1199,8 @@ constexpr int sk_stages() {
 #endif
 template <int BN, int MT>
 constexpr int chain_attn_stages() {
-  return (BN == 16 && MT <= 8) ? ASTRAEA_CHAIN_ATTN_STAGES_SMALL : ASTRAEA_CHAIN_ATTN_STAGES;
+  return (BN == 16 && MT <= 4) ? ASTRAEA_CHAIN_ATTN_STAGES_SMALL
+         : (BN == 16 && MT == 8) ? 2 : ASTRAEA_CHAIN_ATTN_STAGES;
 }
 
 template <int BN, bool DEEP, int MT>
@@ -1499,9 +1436,6 @@ static int run_chain(int M, int nph, const astraea_gemm_phase* ph, void* ws, siz
   a.counters = (int*)ws;
   a.phase_ctr = (int*)((char*)ws + kCounterBytes);
   a.ws = (float*)((char*)ws + kHeadBytes);
-  a.tile_flag = (int*)((char*)ws + kCounterBytes + kPhaseBytes + kAttnWsBytes);
-  a.head_flag = a.tile_flag + kMaxPhases * kMaxFlagTiles;
-  a.head_ctr = a.head_flag + kMaxAttn * 64;
   a.nattn = 0;
   a.pf_layer = -1;
   if (nattn < 0 || nattn > kMaxAttn || (nattn && (!ats || !attn_before || !deep))) return ASTRAEA_EINVAL;
@@ -1514,8 +1448,6 @@ static int run_chain(int M, int nph, const astraea_gemm_phase* ph, void* ws, siz
         (k && attn_before[k] <= attn_before[k - 1]))
       return ASTRAEA_EINVAL;
     const int G = at->num_q_heads / g.num_kv_heads, D = g.head_dim;
-    a.attn_cols[k] = G * D;
-    if (g.num_kv_heads > 64) return ASTRAEA_EUNSUPPORTED;
     a.attn_kind[k] = (D == 128 && G == 4) ? 1 : (D == 64 && G == 2) ? 2 : (D == 64 && G == 4) ? 3
                    : (D == 128 && G == 8) ? 4 : 0;   // 4: a Llama-3-70B TP=8 rank (8 q heads on 1 kv head)
     if (!a.attn_kind[k] || num_sms() > 192) return ASTRAEA_EUNSUPPORTED;

@@ -185,10 +185,6 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   return v;
 }
 
-__device__ __forceinline__ void st_release_i32(int* p, int v) {
-  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 __device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
   int prev;
   asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], %2;" : "=r"(prev) : "l"(p), "r"(v) : "memory");

@@ -26,6 +26,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--batch", type=int, nargs="+", default=[1, 4, 8, 16, 32])
 ap.add_argument("--ctx", type=int, default=673)
 ap.add_argument("--no-step", action="store_true")
+ap.add_argument("--no-step-standalone", action="store_true", help="only the fused step")
 a = ap.parse_args()
 cfg = PRESETS["llama3-8b"]
 hbm = json.loads((Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs", 6650.0) \
@@ -78,7 +79,7 @@ for B in a.batch:
         pos = torch.full((B,), C - 1, dtype=torch.int32, device="cuda")
         slots = table[:, (C - 1) // 16] * 16 + (C - 1) % 16
         keys = torch.zeros(B, dtype=torch.int64, device="cuda")
-        for fuse in (True, False):
+        for fuse in ((True,) if a.no_step_standalone else (True, False)):
             runner.fuse_attention = fuse
             runner.fuse_max_batch = 64
             ms = timed(lambda: runner.decode(tok, pos, slots, table, ctxd, keys_out=keys), 10)
