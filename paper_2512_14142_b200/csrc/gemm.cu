@@ -617,6 +617,7 @@ struct ChainArgs {
   int pf_layer;                // >= 0: prefetch that layer's K/V pages into L2 during the last phase
   int attn_early;              // the first attention's work split runs before griddepcontrol.wait
   int block_rows;              // attention (AS > 1): rows of one pool block in ChainMaps::pool
+  int trace_phase;             // diagnostics: the phase whose split-tile finishers are traced
   SkPhase ph[kMaxPhases];
 };
 constexpr int kAttnCtr = kMaxPhases + 2;   // phase_ctr slots kAttnCtr + k: CTAs done with attention k
@@ -983,9 +984,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
         unsigned long long* tpart = wsq + ((tile * P.maxseg) * (long long)args.M) * kBM + row;
         constexpr bool kPreRes = BN <= 32;   // register budget: BN = 64 reads the residual in the epilogue
         float res[BN], acc[BN];
-        // diagnostics (phase 2, the last finished tile): [11] collect start, [12] collect done,
+        // diagnostics (phase trace_phase, the last finished tile): [11] collect start, [12] collect done,
         // [13] own MMAs done, [14] epilogue done
-        const bool ftr = tr && finisher && !whole && p == 2 && threadIdx.x == 64;
+        const bool ftr = tr && finisher && !whole && p == args.trace_phase && threadIdx.x == 64;
         if (ftr) tr[11] = gtimer();
         if (finisher) {
           if (kPreRes && resid) {
@@ -1043,7 +1044,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
           for (int t = 0; t < MT; ++t) v[t] = acc[t] + v[t];
         }
         sk_finish<BN, SkPhase, MT>(P, (int)tile, row, v, rs, xch, red, (kPreRes && resid) ? res : nullptr, stage ? slot_s : nullptr,
-                      cs_s);
+                      cs_s, ftr ? tr + 30 : nullptr);
         if (ftr) tr[14] = gtimer();
       }
       // phase p done in this CTA: publish (release) for the other CTAs. The
@@ -1483,6 +1484,11 @@ static int run_chain(int M, int nph, const astraea_gemm_phase* ph, void* ws, siz
   }
   a.nattn = nattn;
   a.block_rows = 0;
+  static const int trace_phase = [] {
+    const char* e = getenv("ASTRAEA_TRACE_PHASE");
+    return e ? atoi(e) : 2;
+  }();
+  a.trace_phase = trace_phase;
   if (nattn > 0) {
     // the TMA-staged attention instantiations (AS > 1) read pages through
     // this map; every attention of a launch uses the same pool

@@ -231,7 +231,9 @@ __device__ __forceinline__ void warp_multi_sum(float* v, int lane, float* out) {
 template <int BN, typename A, int MT = BN>
 __device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* v, const float* rs,
                                           bf16* xch, float* red, const float* res_pre = nullptr,
-                                          const int* slot_s = nullptr, const float2* cs_s = nullptr) {
+                                          const int* slot_s = nullptr, const float2* cs_s = nullptr,
+                                          unsigned long long* ftr = nullptr) {
+  // ftr (diagnostics, thread row 0 only): [0] exchange written, [1] stores issued
   // slot_s / cs_s (optional): the tokens' pool slots and the [M][D/2] RoPE
   // table staged in shared memory by the caller (QKV_ROPE)
   const Epi& e = a.epi;
@@ -242,27 +244,35 @@ __device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* 
 #pragma unroll
     for (int t = 0; t < MT; ++t) v[t] *= rs[t];
   }
+  // (as in the QKV path below: pointers and strides into registers before the
+  // token loops, so the parameter-space program is not re-read behind the stores)
+  bf16* __restrict__ cbase = a.C;
+  const long long ldc = a.ldc;
   if (e.kind == EPI_ARGMAX) {
+    unsigned long long* __restrict__ amax = e.amax;
+    const int col = f + e.amax_off;
 #pragma unroll
     for (int t = 0; t < MT; ++t) {
       if (t >= M) break;
-      if (a.C && fok) a.C[(long long)t * a.ldc + f] = f2bf(v[t]);
-      const unsigned long long k = warp_max64(fok ? argmax_key(v[t], f + e.amax_off) : 0ull);
-      if ((row & 31) == 0) atomicMax(e.amax + t, k);
+      if (cbase && fok) cbase[t * ldc + f] = f2bf(v[t]);
+      const unsigned long long k = warp_max64(fok ? argmax_key(v[t], col) : 0ull);
+      if ((row & 31) == 0) atomicMax(amax + t, k);
     }
     return;
   }
   if (e.kind == EPI_NONE || e.kind == EPI_RESIDUAL) {
     float sq[BN];
+    const bool resid = e.kind == EPI_RESIDUAL;
+    const bf16* __restrict__ rbase = e.residual;
 #pragma unroll
     for (int t = 0; t < MT; ++t) {
       sq[t] = 0.f;
       if (t < M && fok) {
         float o = v[t];
-        if (e.kind == EPI_RESIDUAL)   // preloaded by the caller, or from L2 (produced by other CTAs)
-          o += res_pre ? res_pre[t] : bf2f(__ldcg(e.residual + (long long)t * a.ldc + f));
+        if (resid)   // preloaded by the caller, or from L2 (produced by other CTAs)
+          o += res_pre ? res_pre[t] : bf2f(__ldcg(rbase + t * ldc + f));
         const bf16 ob = f2bf(o);
-        a.C[(long long)t * a.ldc + f] = ob;
+        cbase[t * ldc + f] = ob;
         sq[t] = bf2f(ob) * bf2f(ob);
       }
     }
@@ -285,35 +295,68 @@ __device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* 
 #pragma unroll
   for (int t = 0; t < MT; ++t) xch[t * kBM + row] = f2bf(v[t]);
   epi_bar();
+  if (ftr) ftr[0] = gtimer();
   if (e.kind == EPI_SILU) {
     if (row >= 64) {
       const int out_f = tile * 64 + (row - 64);
       if (fok) {
+        bf16* __restrict__ cs = cbase + out_f;
 #pragma unroll
         for (int t = 0; t < MT; ++t)
           if (t < M)
-            a.C[(long long)t * a.ldc + out_f] = f2bf(silu_rounded(bf2f(xch[t * kBM + row - 64])) * bf2f(xch[t * kBM + row]));
+            cs[t * ldc] = f2bf(silu_rounded(bf2f(xch[t * kBM + row - 64])) * bf2f(xch[t * kBM + row]));
       }
     }
   } else {  // QKV_ROPE
-    const int head = f / e.D, hrow = f % e.D, half = e.D / 2;
+    // Everything the token loop needs is read into registers first: the
+    // epilogue program lives in kernel-parameter space and, behind the
+    // loop's global stores, the compiler would re-read it every token
+    // (0.4 us per token at batch 16 before this).
+    const int D = e.D, half = D / 2, Hq = e.Hq, Hkv = e.Hkv;
+    const int head = f / D, hrow = f % D;
     const int partner = row ^ half;
-    const bool rot = head < e.Hq + e.Hkv;
+    const bool rot = head < Hq + Hkv;
+    const int fr = hrow % half;
     if (fok) {
+      if (head < Hq) {
+        bf16* __restrict__ cq = cbase + (long long)head * D + hrow;
 #pragma unroll 4
-      for (int t = 0; t < MT; ++t) {
-        if (t >= M) break;
-        const float x = bf2f(xch[t * kBM + row]);
-        float y = x;
-        if (rot) {
+        for (int t = 0; t < MT; ++t) {
+          if (t >= M) break;
+          const float x = bf2f(xch[t * kBM + row]);
           const float xp = bf2f(xch[t * kBM + partner]);
-          const float2 r = cs_s ? cs_s[t * half + hrow % half] : rope_cs(e, t, hrow % half);
-          y = hrow < half ? x * r.x - xp * r.y : x * r.x + xp * r.y;
+          const float2 r = cs_s ? cs_s[t * half + fr] : rope_cs(e, t, fr);
+          cq[t * ldc] = f2bf(hrow < half ? x * r.x - xp * r.y : x * r.x + xp * r.y);
         }
-        qkv_store(e, a.C, a.ldc, t, head, hrow, y, slot_s ? slot_s[t] : -2);
+      } else {
+        const int kv = head < Hq + Hkv ? 0 : 1;
+        const int h = head - Hq - kv * Hkv;
+        bf16* __restrict__ pool = e.pool;
+        const long long bel = e.block_el;
+        const int bt = e.bt;
+        const long long hoff = ((long long)(e.layer * 2 + kv) * Hkv + h) * bt * D + hrow;
+        const int32_t* __restrict__ gslots = e.slots;
+#pragma unroll 4
+        for (int t = 0; t < MT; ++t) {
+          if (t >= M) break;
+          const float x = bf2f(xch[t * kBM + row]);
+          float y = x;
+          if (rot) {
+            const float xp = bf2f(xch[t * kBM + partner]);
+            const float2 r = cs_s ? cs_s[t * half + fr] : rope_cs(e, t, fr);
+            y = hrow < half ? x * r.x - xp * r.y : x * r.x + xp * r.y;
+          }
+          const int slot = slot_s ? slot_s[t] : gslots[t];
+          if (slot >= 0) {
+            const int blk = bt == 16 ? slot >> 4 : slot / bt;   // 16-token pages: no integer division
+            const int off = bt == 16 ? slot & 15 : slot % bt;
+            pool[(long long)blk * bel + hoff + (long long)off * D] = f2bf(y);
+          }
+        }
       }
     }
   }
+  if (ftr) ftr[1] = gtimer();
   epi_bar();
 }
 

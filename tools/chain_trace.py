@@ -20,6 +20,7 @@ ap.add_argument("--ctx", type=int, default=900)
 ap.add_argument("--layers", type=int, nargs="+", default=[0, 1, 2, 16, 31])
 ap.add_argument("--no-fuse", action="store_true")
 ap.add_argument("--per-cta", action="store_true")
+ap.add_argument("--chain-layers", type=int, default=1)
 a = ap.parse_args()
 cfg = PRESETS["llama3-8b"]
 w = LlamaWeights(cfg)
@@ -27,6 +28,7 @@ B, nb = a.batch, (a.ctx + 16) // 16
 pool = KvPool(cfg, B * nb + 4)
 r = LlamaRunner(w, pool)
 r.fuse_attention = not a.no_fuse
+r.chain_layers = a.chain_layers
 table = torch.arange(B * nb, dtype=torch.int32, device="cuda").view(B, nb)
 tok = torch.zeros(B, dtype=torch.int32, device="cuda")
 pos = torch.full((B,), a.ctx, dtype=torch.int32, device="cuda")
@@ -75,17 +77,25 @@ for i in range(n):
         att["m_group0_spins_max"] = int(sp.max())
         print(json.dumps({"layer": li, "attention_warp0_first_piece": att}))
 
-# split-tile finishers of the down projection (phase 2): collect / own MMAs / epilogue
+# split-tile finishers of phase ASTRAEA_TRACE_PHASE (default 2, down): collect / own MMAs / epilogue
+import os
+tp = int(os.environ.get("ASTRAEA_TRACE_PHASE", "2"))
 i = a.layers[-1] + 1
 s = t[i]
 fm = s[:, 11] > 0
 if bool(fm.any()):
-    rel = float(s[:, 3][s[:, 3] > 0].median())   # down activations released
+    f = s[fm]
+    d = lambda k1, k0: round(float((f[:, k1] - f[:, k0]).median()) / 1000, 2)  # noqa: E731
+    print(json.dumps({"phase": tp, "finishers": int(fm.sum()), "epilogue_us": d(14, 13),
+                      "exchange_us": d(30, 13), "loop_us": d(31, 30)}))
+if bool(fm.any()) and tp < 4:
+    rel = float(s[:, 1 + tp][s[:, 1 + tp] > 0].median())   # the phase's activations released
     f = s[fm]
     g = lambda k: [round(float((f[:, k] - rel).median()) / 1000, 2), round(float((f[:, k] - rel).max()) / 1000, 2)]  # noqa: E731
-    print(json.dumps({"down_finishers": int(fm.sum()), "collect_start": g(11), "collect_done": g(12),
-                      "own_mma_done": g(13), "epilogue_done": g(14),
-                      "others_done_median": round(float((s[~fm][:, 7] - rel).median()) / 1000, 2)}))
+    print(json.dumps({"phase": tp, "finishers": int(fm.sum()), "collect_start": g(11), "collect_done": g(12),
+                      "own_mma_done": g(13), "xch_done": g(30), "stores_done": g(31), "epilogue_done": g(14),
+                      "others_done_median": round(float((s[~fm][:, 5 + tp] - rel).median()) / 1000, 2),
+                      "all_done_max": round(float((s[:, 5 + tp] - rel).max()) / 1000, 2)}))
 
 if a.per_cta:
     # per-CTA phase completion (relative to the phase's activation release) of one launch

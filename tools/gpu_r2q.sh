@@ -1,0 +1,8 @@
+for v in main ring224 main ring224; do
+  if [ $v = main ]; then unset ASTRAEA_LIB; else export ASTRAEA_LIB=$PWD/paper_2512_14142_b200/lib/variants/$v/libastraea_b200.so; fi
+  echo "== $v"; timeout 600 python tools/attn_ab.py --batch 1 2 4 8 16 --no-step-standalone 2>&1 | grep "^{" | python -c "
+import sys,json
+for l in sys.stdin:
+    d=json.loads(l); print(d['batch'], 'fused %.3f ms (%.3f)'%(d['step_ms_fused'], d['step_frac_fused']))
+"
+done

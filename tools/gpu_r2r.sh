@@ -1,0 +1,8 @@
+ASTRAEA_TRACE_PHASE=3 timeout 300 python tools/chain_trace.py --batch 16 --ctx 673 --layers 16 2>&1 | grep epilogue_us
+ASTRAEA_TRACE_PHASE=0 timeout 300 python tools/chain_trace.py --batch 16 --ctx 673 --layers 16 2>&1 | grep epilogue_us
+timeout 900 python -m pytest tests/test_gpu_8b.py tests/test_gpu_model.py tests/test_gpu_kernels.py -x -q 2>&1 | tail -2
+timeout 600 python tools/attn_ab.py --batch 1 4 8 16 32 --no-step-standalone 2>&1 | grep "^{" | python -c "
+import sys,json
+for l in sys.stdin:
+    d=json.loads(l); print(d['batch'], 'fused %.3f ms (%.3f)'%(d['step_ms_fused'], d['step_frac_fused']))
+"
