@@ -994,6 +994,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
 #pragma unroll
             for (int t = 0; t < MT; ++t)
               res[t] = (t < args.M && f < P.N) ? bf2f(__ldcg(P.epi.residual + (long long)t * P.ldc + f)) : 0.f;
+            // pin the loads here (issued before the collect, consumed after it):
+            // the compiler would otherwise sink them into the epilogue loop and
+            // pay an L2 round trip there
+#pragma unroll
+            for (int t = 0; t < MT; ++t) asm volatile("" : "+f"(res[t]));
           }
 #pragma unroll
           for (int t = 0; t < MT; ++t) acc[t] = 0.f;
@@ -1030,6 +1035,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
+        if (ftr) tr[30] = gtimer();   // accumulator read back from TMEM
         if (!finisher) {
           unsigned long long* pp = tpart + (long long)(cta - c_first) * args.M * kBM;
 #pragma unroll
@@ -1043,8 +1049,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
 #pragma unroll
           for (int t = 0; t < MT; ++t) v[t] = acc[t] + v[t];
         }
+        if (ftr) tr[31] = gtimer() + (v[0] == 1234.5f);   // partials added
         sk_finish<BN, SkPhase, MT>(P, (int)tile, row, v, rs, xch, red, (kPreRes && resid) ? res : nullptr, stage ? slot_s : nullptr,
-                      cs_s, ftr ? tr + 30 : nullptr);
+                      cs_s, ftr ? tr + 28 : nullptr);
         if (ftr) tr[14] = gtimer();
       }
       // phase p done in this CTA: publish (release) for the other CTAs. The
@@ -1600,7 +1607,13 @@ extern "C" int astraea_gemm_bf16_ex(const void* A, int32_t lda, const void* W, i
   a.K = K;
   a.ldc = ldc;
   a.epi = e;
-  if (pair_gemm_enabled()) {
+  // Short prefills (recompute-on-resume appends) are weight-streaming bound:
+  // there the one-CTA 128-row tiles keep more SMs streaming than 256x256
+  // CTA-pair tiles -- K = 4096 projections at M <= 128 (gate/up included)
+  // and N <= 6144 ones (QKV, O) at M <= 256 (tools/gpu_r2t.sh sweep: 128
+  // tokens 50 -> 37 us QKV, 37.5 -> 31.8 O, 90.5 -> 76 gate/up per layer).
+  const bool short_rows = K <= 4096 && (M <= 128 || (M <= 256 && N <= 6144));
+  if (pair_gemm_enabled() && !short_rows) {
     if ((rc = make_map(&ma, A, M, K, lda, 128))) return rc;
     if ((rc = make_map(&mb, W, N, K, ldw, 128))) return rc;
     a.splits = pair_splits(M, N, K);

@@ -276,6 +276,7 @@ __device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* 
         sq[t] = bf2f(ob) * bf2f(ob);
       }
     }
+    if (ftr) ftr[0] = gtimer();
     if (e.ssq_out) {
       const int q = row >> 5, lane = row & 31;
       if constexpr (MT <= 32) {
@@ -288,6 +289,7 @@ __device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* 
       if (row < M) e.ssq_out[(long long)tile * M + row] = red[row] + red[BN + row] + red[2 * BN + row] + red[3 * BN + row];
       epi_bar();
     }
+    if (ftr) ftr[1] = gtimer();
     return;
   }
   // pair exchange through shared memory (values rounded to bf16, as the

@@ -87,7 +87,8 @@ if bool(fm.any()):
     f = s[fm]
     d = lambda k1, k0: round(float((f[:, k1] - f[:, k0]).median()) / 1000, 2)  # noqa: E731
     print(json.dumps({"phase": tp, "finishers": int(fm.sum()), "epilogue_us": d(14, 13),
-                      "exchange_us": d(30, 13), "loop_us": d(31, 30)}))
+                      "tmem_ld_us": d(30, 13), "acc_add_us": d(31, 30), "to_mark0_us": d(28, 31),
+                      "mark0_to_mark1_us": d(29, 28), "tail_us": d(14, 29)}))
 if bool(fm.any()) and tp < 4:
     rel = float(s[:, 1 + tp][s[:, 1 + tp] > 0].median())   # the phase's activations released
     f = s[fm]
