@@ -6,7 +6,7 @@ the 64-request synthetic agent trace of the reference generator
 category mix, workload.py:390-433); Stateful-MLFQ + adaptive Preserve/Swap/
 Discard, KV capacity 12,000 tokens per GPU (the 0.3 level of the survey's
 40,000-token grid, 131,072 B/token), parallel-max; cost tables measured on the
-B200 (profiles/r1_b200_cost_tables.json). The scheduler, KV policy and event
+B200 (profiles/r2_b200_cost_tables.json). The scheduler, KV policy and event
 loop are the unmodified reference (``agentsched``), with the device attached
 through ``paper_2512_14142_b200.plugin``; model clock, so every decision is
 the reference's and the replay's report bytes are asserted equal to the
@@ -58,6 +58,8 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
 METRIC = "avg/p99 JCT and req/s on synthetic agent trace; KV swap GB/s; decode HBM GB/s"
+# cost tables measured on the B200 with this round's kernels (tools/calibrate.py)
+CAL_TABLES = ROOT / "profiles" / "r2_b200_cost_tables.json"
 
 
 def parse(argv=None):
@@ -74,7 +76,7 @@ def parse(argv=None):
                     help="K1/K2 path (tools/swap_load.py: staged keeps the host link at ~54 GB/s and slows a "
                          "concurrent decode by ~4%%; the zero-copy SM kernel slows it 2x)")
     ap.add_argument("--cost-tables", choices=("calibrated", "b200-like", "reference"), default="calibrated",
-                    help="scheduler cost tables: measured on the B200 (profiles/r1_b200_cost_tables.json), "
+                    help="scheduler cost tables: measured on the B200 (profiles/r2_b200_cost_tables.json), "
                          "the survey's B200-like guess, or the reference defaults")
     ap.add_argument("--placement", choices=("free-tokens", "round-robin"), default="free-tokens",
                     help="multi-GPU: requests placed at arrival on the replica with the most free KV "
@@ -112,7 +114,7 @@ def build_workload(args, rank, world):
     full.sort(key=lambda r: (r.arrival_time, r.id))
     tables = getattr(args, "cost_tables", "calibrated")
     if tables == "calibrated":
-        pred, cal = scenarios.calibrated_predictor(ns)
+        pred, cal = scenarios.calibrated_predictor(ns, CAL_TABLES)
         args.swap_tokens_per_s = float(cal["swap_bandwidth_tokens_per_s"])
     elif tables == "b200-like":
         pred = scenarios.b200_like_predictor(ns)

@@ -84,7 +84,7 @@ def calibrate(dp, prefill_points=(128, 256, 512, 1024, 2048), decode_batches=(1,
         "decode_step_seconds_by_batch": {str(k): v for k, v in decode.items()},
         "decode_ctx": decode_ctx,
         "swap": {"tokens": swap_tokens, "out_s": t_out, "in_s": t_in,
-                 "mode": "kernel" if dp.swap_mode == L.SWAP_KERNEL else "dma"},
+                 "mode": {L.SWAP_KERNEL: "kernel", L.SWAP_DMA: "dma", L.SWAP_STAGED: "staged"}[dp.swap_mode]},
     }
 
 

@@ -99,8 +99,10 @@ def b200_like_predictor(ns):
                                    decode=ns.DecodeModel(0.006))
 
 
-def calibrated_predictor(ns):
-    cal = json.loads(CALIBRATION.read_text())
+def calibrated_predictor(ns, path=None):
+    """ServiceTimePredictor from B200-measured tables (default: the round-1
+    tables the c1cal goldens were generated with)."""
+    cal = json.loads((path or CALIBRATION).read_text())
     cfg = dict(cal["predictor"])
     cfg["api_latency_means"] = ns.ServiceTimePredictor().to_config()["api_latency_means"]
     return ns.ServiceTimePredictor.from_config(cfg), cal

@@ -46,7 +46,7 @@ def trace(qps, n):
 
 def cell(wl, capacity, tables, dp):
     if tables == "calibrated":
-        pred, cal = scenarios.calibrated_predictor(host)
+        pred, cal = scenarios.calibrated_predictor(host, ROOT / "profiles" / "r2_b200_cost_tables.json")
         bw = float(cal["swap_bandwidth_tokens_per_s"])
     else:
         pred, bw = host.ServiceTimePredictor(), 20_000.0
