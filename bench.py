@@ -574,6 +574,9 @@ def bench_engine():
 
 def main():
     args = parse()
+    if os.environ.get("ASTRAEA_BENCH_TRACEBACK_S"):   # diagnostics: dump every thread's stack on a hang
+        import faulthandler
+        faulthandler.dump_traceback_later(int(os.environ["ASTRAEA_BENCH_TRACEBACK_S"]), exit=True)
     if args.impl == "reference":
         return run_reference(args)
     import torch

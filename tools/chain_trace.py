@@ -89,6 +89,12 @@ if bool(fm.any()):
     print(json.dumps({"phase": tp, "finishers": int(fm.sum()), "epilogue_us": d(14, 13),
                       "tmem_ld_us": d(30, 13), "acc_add_us": d(31, 30), "to_mark0_us": d(28, 31),
                       "mark0_to_mark1_us": d(29, 28), "tail_us": d(14, 29)}))
+if bool(fm.any()) and os.environ.get("TRACE_FINISHERS"):
+    base14 = float(s[:, 1 + tp][s[:, 1 + tp] > 0].median()) if tp < 4 else float(s[fm][:, 13].min())
+    idx = torch.nonzero(fm).view(-1).tolist()
+    rows = sorted(((int(c), [round(float(s[c, k] - base14) / 1000, 2) for k in (11, 12, 13, 28, 29, 14)]) for c in idx),
+                  key=lambda r: -r[1][-1])
+    print(json.dumps({"phase": tp, "finishers_by_done (cta, [collect_start, collect_done, own_mma, mark0, mark1, done])": rows[:10] + rows[-3:]}))
 if bool(fm.any()) and tp < 4:
     rel = float(s[:, 1 + tp][s[:, 1 + tp] > 0].median())   # the phase's activations released
     f = s[fm]
