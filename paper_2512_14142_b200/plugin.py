@@ -210,6 +210,20 @@ def engine_classes(ns=None):
     return GpuKvCacheManager, GpuEngine
 
 
+def report_json_with_device(report) -> str:
+    """RunReport v1 JSON (metrics.py:115-126) with the device counters under
+    ``audits["device"]`` -- opt-in: the default
+    ``report.to_json()`` stays byte-identical to the reference, this one
+    still loads with the reference's ``RunReport.from_dict`` so its
+    ``gantt`` / ``compare`` tooling (cli.py:561-721) works on B200 runs."""
+    import json
+    d = report.to_dict()
+    dev = getattr(report, "device", None)
+    if dev is not None:
+        d["audits"] = dict(d["audits"], device=dict(dev))
+    return json.dumps(d, sort_keys=True, indent=2)
+
+
 def run_on_gpu(workload, policy, predictor, memory, config, datapath, clock: str = "model", ns=None):
     """The reference's ``run()`` (simulator.py:484-494) with the B200 data
     path attached."""

@@ -90,3 +90,22 @@ def test_pool_size_check_bounds_by_capacity_and_trace():
     rec.pool.num_blocks += 1
     wl, pol, pred, mem, cfg = scenarios.build(ref, "c1b200/6000")
     GpuEngine(wl, pol, pred, mem, cfg, rec)
+
+
+def test_report_with_device_audits_loads_in_the_reference():
+    """Opt-in export: the device counters under
+    audits["device"]; the reference's RunReport.from_dict and compare()
+    accept it, and everything but that key equals the default bytes."""
+    import json
+    name = "c1b200/6000"
+    wl, pol, pred, mem, cfg = scenarios.build(ref, name)
+    rep = plugin.run_on_gpu(wl, pol, pred, mem, cfg, Recorder())
+    js = plugin.report_json_with_device(rep)
+    d = json.loads(js)
+    assert d["audits"]["device"]["batches"] == rep.device["batches"]
+    back = ref.RunReport.from_dict(d)
+    assert back.audits["device"]["clock"] == "model"
+    del d["audits"]["device"]
+    assert ref.RunReport.from_dict(d).to_json() == rep.to_json()
+    table = ref.compare({"b200": back, "reference": scenarios.run_scenario(ref, name)}, baseline="reference")
+    assert table is not None
