@@ -62,6 +62,9 @@ struct GemmArgs {
   int splits;
   unsigned long long* part;    // [tiles][splits - 1][2 CTAs][128][256] tagged fp32 partials
   int* ctr;                    // workspace counters: [kMaxPhases] exit, [kMaxPhases + 1] launch epoch
+  // one-CTA kernel split-K (short prefills): K cut into gridDim.z ranges
+  float* rpart;                // [tiles][splits][128][BN] fp32 partials
+  int* rctr;                   // [tiles] arrival counters (zero between uses)
 };
 
 // Epilogue of one 128-row x BN-column accumulator tile: thread = token row m
@@ -229,7 +232,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile_a = blockIdx.x;   // tokens (128)
   const int tile_b = blockIdx.y;   // output columns (BN)
-  const int nkb = (args.K + kBK - 1) / kBK;
+  // split-K: this CTA's k-block range (gridDim.z splits of the K dimension)
+  const int nkb_all = (args.K + kBK - 1) / kBK;
+  const int S = gridDim.z, z = blockIdx.z;
+  const int kb0 = (int)((long long)z * nkb_all / S), kb1 = (int)((long long)(z + 1) * nkb_all / S);
+  const int nkb = kb1 - kb0;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
@@ -253,16 +260,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int pre = min(nkb, STAGES);
       for (int i = 0; i < pre; ++i) {  // weights first, before the dependency wait
         mbar_arrive_expect_tx(&full[i], A_BYTES + B_BYTES);
-        tma_load_2d(sb + i * B_BYTES, &map_b, &full[i], i * kBK, tile_b * BN);
+        tma_load_2d(sb + i * B_BYTES, &map_b, &full[i], (kb0 + i) * kBK, tile_b * BN);
       }
       pdl_wait();
-      for (int i = 0; i < pre; ++i) tma_load_2d(sa + i * A_BYTES, &map_a, &full[i], i * kBK, tile_a * kBM);
+      for (int i = 0; i < pre; ++i) tma_load_2d(sa + i * A_BYTES, &map_a, &full[i], (kb0 + i) * kBK, tile_a * kBM);
       for (int i = pre; i < nkb; ++i) {
         const int s = i % STAGES;
         mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
         mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
-        tma_load_2d(sa + s * A_BYTES, &map_a, &full[s], i * kBK, tile_a * kBM);
-        tma_load_2d(sb + s * B_BYTES, &map_b, &full[s], i * kBK, tile_b * BN);
+        tma_load_2d(sa + s * A_BYTES, &map_a, &full[s], (kb0 + i) * kBK, tile_a * kBM);
+        tma_load_2d(sb + s * B_BYTES, &map_b, &full[s], (kb0 + i) * kBK, tile_b * BN);
       }
     }
   } else if (warp == 1) {
@@ -292,7 +299,62 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_wait(done, 0);
     tc_fence_after();
     const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
-    rows_epilogue<BN>(args, m, mok, rs, lane_addr, tile_b);
+    bool finish = true;
+    if (S > 1) {
+      // every split publishes its fp32 partial; the last to arrive sums all
+      // of them in split order (deterministic) back into its TMEM tile and
+      // runs the epilogue
+      const int row = quarter * 32 + lane;
+      const long long tile = (long long)tile_a * gridDim.y + tile_b;
+      float* mine = args.rpart + ((tile * S + z) * kBM + row) * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tmem_ld32(lane_addr + c, v);
+#pragma unroll
+        for (int k = 0; k < 32; k += 4)
+          __stcg(reinterpret_cast<float4*>(mine + c + k), make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]));
+      }
+      __threadfence();
+      epi_bar();
+      __shared__ int s_last;
+      if (threadIdx.x == 64) s_last = atom_add_acq_rel(args.rctr + tile, 1) == S - 1;
+      epi_bar();
+      finish = s_last;
+      if (finish) {
+        __threadfence();
+        const float* base = args.rpart + (tile * S * kBM + row) * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          float sum[32], own[32];
+          tmem_ld32(lane_addr + c, own);
+#pragma unroll
+          for (int k = 0; k < 32; ++k) sum[k] = 0.f;
+          for (int zz = 0; zz < S; ++zz) {
+            if (zz == z) {
+#pragma unroll
+              for (int k = 0; k < 32; ++k) sum[k] += own[k];
+            } else {
+              const float* src = base + (long long)zz * kBM * BN + c;
+#pragma unroll
+              for (int k = 0; k < 32; k += 4) {
+                const float4 w = __ldcg(reinterpret_cast<const float4*>(src + k));
+                sum[k] += w.x;
+                sum[k + 1] += w.y;
+                sum[k + 2] += w.z;
+                sum[k + 3] += w.w;
+              }
+            }
+          }
+          tmem_st32(lane_addr + c, sum);
+        }
+        tc_fence_before();
+        epi_bar();
+        tc_fence_after();
+        if (threadIdx.x == 64) args.rctr[tile] = 0;
+      }
+    }
+    if (finish) rows_epilogue<BN>(args, m, mok, rs, lane_addr, tile_b);
   }
   tc_fence_before();
   __syncthreads();
@@ -1408,6 +1470,34 @@ static int pair_splits(int M, int N, int K) {
   if (tiles >= pairs) return 1;
   return std::max(1, std::min(std::min(pairs / tiles, kb / min_kbs), 8));
 }
+// One-CTA kernel plan for short prefills: BN and the split-K count that fill
+// the SMs (>= 8 k-blocks per split, <= 4 splits).
+struct RowsPlan {
+  int bn, splits;
+};
+static RowsPlan rows_plan(int M, int N, int K) {
+  RowsPlan p;
+  p.bn = (N % 256 == 0 && (long long)((M + kBM - 1) / kBM) * (N / 256) >= num_sms()) ? 256 : 128;
+  const long long tiles = (long long)((M + kBM - 1) / kBM) * ((N + p.bn - 1) / p.bn);
+  const int nkb = (K + kBK - 1) / kBK;
+  static const int max_splits = [] {
+    const char* e = getenv("ASTRAEA_ROWS_SPLITS");
+    return e ? std::max(1, std::min(8, atoi(e))) : 2;   // 128-token prefill 6.78 -> 6.68 ms; 4: no better
+  }();
+  int s = 1;
+  if (tiles < num_sms()) s = (int)std::min<long long>(num_sms() / tiles, max_splits);   // one wave
+  s = std::max(1, std::min(s, nkb / 8));
+  p.splits = s;
+  return p;
+}
+static bool short_rows(int M, int N, int K) { return K <= 4096 && (M <= 128 || (M <= 256 && N <= 6144)); }
+static size_t rows_partial_bytes(int M, int N, int K) {
+  const RowsPlan p = rows_plan(M, N, K);
+  if (p.splits <= 1) return 0;
+  const long long tiles = (long long)((M + kBM - 1) / kBM) * ((N + p.bn - 1) / p.bn);
+  return (size_t)tiles * p.splits * kBM * p.bn * sizeof(float);
+}
+
 static size_t pair_partial_bytes(int M, int N, int K) {
   const int S = pair_splits(M, N, K);
   const long long tiles = (long long)((M + 255) / 256) * ((N + 255) / 256);
@@ -1417,7 +1507,7 @@ static size_t pair_partial_bytes(int M, int N, int K) {
 extern "C" size_t astraea_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K) {
   if (M <= 0 || N <= 0 || K <= 0) return 0;
   if (M > kColsMaxM) {
-    const size_t p = pair_partial_bytes(M, N, K);
+    const size_t p = short_rows(M, N, K) ? rows_partial_bytes(M, N, K) : pair_partial_bytes(M, N, K);
     return p ? kHeadBytes + p : 0;
   }
   return kHeadBytes + partial_bytes(M, sk_plan(M, N, K));
@@ -1612,8 +1702,11 @@ extern "C" int astraea_gemm_bf16_ex(const void* A, int32_t lda, const void* W, i
   // CTA-pair tiles -- K = 4096 projections at M <= 128 (gate/up included)
   // and N <= 6144 ones (QKV, O) at M <= 256 (tools/gpu_r2t.sh sweep: 128
   // tokens 50 -> 37 us QKV, 37.5 -> 31.8 O, 90.5 -> 76 gate/up per layer).
-  const bool short_rows = K <= 4096 && (M <= 128 || (M <= 256 && N <= 6144));
-  if (pair_gemm_enabled() && !short_rows) {
+  const bool rows_short = short_rows(M, N, K);
+  a.splits = 1;
+  a.rpart = nullptr;
+  a.rctr = nullptr;
+  if (pair_gemm_enabled() && !rows_short) {
     if ((rc = make_map(&ma, A, M, K, lda, 128))) return rc;
     if ((rc = make_map(&mb, W, N, K, ldw, 128))) return rc;
     a.splits = pair_splits(M, N, K);
@@ -1629,10 +1722,21 @@ extern "C" int astraea_gemm_bf16_ex(const void* A, int32_t lda, const void* W, i
     }
     return launch_pair<6>(ma, mb, a, st);
   }
-  const int bn = (N % 256 == 0 && (long long)((M + kBM - 1) / kBM) * (N / 256) >= num_sms()) ? 256 : 128;
+  const RowsPlan rp = rows_plan(M, N, K);
+  const int bn = rp.bn;
+  int splits = rows_short ? rp.splits : 1;
+  const long long rtiles = (long long)((M + kBM - 1) / kBM) * ((N + bn - 1) / bn);
+  if (splits > 1) {
+    if (ws && ws_bytes >= kHeadBytes + rows_partial_bytes(M, N, K) && rtiles * sizeof(int) <= kCounterBytes) {
+      a.rpart = (float*)((char*)ws + kHeadBytes);
+      a.rctr = (int*)ws;   // the tile counters (zero between uses, as for the chain)
+    } else {
+      splits = 1;          // no workspace: unsplit (fewer SMs busy, same result)
+    }
+  }
   if ((rc = make_map(&ma, A, M, K, lda, kBM))) return rc;
   if ((rc = make_map(&mb, W, N, K, ldw, bn))) return rc;
-  dim3 grid((M + kBM - 1) / kBM, (N + bn - 1) / bn, 1);
+  dim3 grid((M + kBM - 1) / kBM, (N + bn - 1) / bn, splits);
   if (bn == 256) return launch_rows<256, 4>(ma, mb, a, grid, st);
   return launch_rows<128, 6>(ma, mb, a, grid, st);
 }
