@@ -335,7 +335,23 @@ __device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* 
     const int partner = row ^ half;
     const bool rot = head < Hq + Hkv;
     const int fr = hrow % half;
-    if (fok) {
+    // The (cos, sin) source is chosen once, outside the token loops: with a
+    // per-token `cs_s ? table : rope_cs()` the compiler may evaluate the
+    // sincos/pow fallback speculatively for every token.
+    const float2* __restrict__ cst = cs_s ? cs_s : e.cs;
+    if (fok && !cst) {
+#pragma unroll 1
+      for (int t = 0; t < M; ++t) {   // no table at all (not used by the runners): compute in place
+        const float x = bf2f(xch[t * kBM + row]);
+        float y = x;
+        if (rot) {
+          const float xp = bf2f(xch[t * kBM + partner]);
+          const float2 r = rope_cs(e, t, fr);
+          y = hrow < half ? x * r.x - xp * r.y : x * r.x + xp * r.y;
+        }
+        qkv_store(e, cbase, ldc, t, head, hrow, y, slot_s ? slot_s[t] : -2);
+      }
+    } else if (fok) {
       if (head < Hq) {
         bf16* __restrict__ cq = cbase + (long long)head * D + hrow;
 #pragma unroll 4
@@ -343,7 +359,7 @@ __device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* 
           if (t >= M) break;
           const float x = bf2f(xch[t * kBM + row]);
           const float xp = bf2f(xch[t * kBM + partner]);
-          const float2 r = cs_s ? cs_s[t * half + fr] : rope_cs(e, t, fr);
+          const float2 r = cst[t * half + fr];
           cq[t * ldc] = f2bf(hrow < half ? x * r.x - xp * r.y : x * r.x + xp * r.y);
         }
       } else {
@@ -353,7 +369,7 @@ __device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* 
         const long long bel = e.block_el;
         const int bt = e.bt;
         const long long hoff = ((long long)(e.layer * 2 + kv) * Hkv + h) * bt * D + hrow;
-        const int32_t* __restrict__ gslots = e.slots;
+        const int32_t* __restrict__ sl = slot_s ? slot_s : e.slots;   // chosen once (no speculative global load)
 #pragma unroll 4
         for (int t = 0; t < MT; ++t) {
           if (t >= M) break;
@@ -361,14 +377,15 @@ __device__ __forceinline__ void sk_finish(const A& a, int tile, int row, float* 
           float y = x;
           if (rot) {
             const float xp = bf2f(xch[t * kBM + partner]);
-            const float2 r = cs_s ? cs_s[t * half + fr] : rope_cs(e, t, fr);
+            const float2 r = cst[t * half + fr];
             y = hrow < half ? x * r.x - xp * r.y : x * r.x + xp * r.y;
           }
-          const int slot = slot_s ? slot_s[t] : gslots[t];
+          const int slot = sl[t];
           if (slot >= 0) {
-            const int blk = bt == 16 ? slot >> 4 : slot / bt;   // 16-token pages: no integer division
-            const int off = bt == 16 ? slot & 15 : slot % bt;
-            pool[(long long)blk * bel + hoff + (long long)off * D] = f2bf(y);
+            if (bt == 16)   // 16-token pages: no integer division
+              pool[(long long)(slot >> 4) * bel + hoff + (long long)(slot & 15) * D] = f2bf(y);
+            else
+              pool[(long long)(slot / bt) * bel + hoff + (long long)(slot % bt) * D] = f2bf(y);
           }
         }
       }
