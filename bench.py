@@ -801,7 +801,7 @@ def chain_kernel_time(dp, cfg, B, ctx, reps=50):
 def profiled_traffic(B):
     """DRAM bytes (read + write) per chain launch from the committed ncu
     --set full capture of the same kernel (profiles/), or None."""
-    p = ROOT / "profiles" / "r1_ncu_chain_traffic.json"
+    p = ROOT / "profiles" / "r2_ncu_chain_traffic.json"
     if not p.exists():
         return None
     d = json.loads(p.read_text())
