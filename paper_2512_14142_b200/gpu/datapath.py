@@ -88,13 +88,19 @@ def _loc(location) -> str:
 class KvDataPath:
     def __init__(self, cfg: LlamaConfig, weights: Optional[LlamaWeights] = None, num_blocks: int = 4096,
                  device="cuda", swap_mode: int = L.SWAP_STAGED, seed: int = 0, measure: bool = False,
-                 token_seed: int = 0):
+                 token_seed: int = 0, runner_factory=None, token_vocab: Optional[int] = None):
+        """``runner_factory(weights, pool)``: the model runner (default
+        LlamaRunner; a tensor-parallel rank passes a TpLlamaRunner over its
+        shard -- every rank then executes the same plans).
+        ``token_vocab``: the vocabulary prompt ids are drawn from (default
+        cfg.vocab; a TP shard config carries only its lm_head slice)."""
         L.require_cuda()
         self.cfg = cfg
         self.device = torch.device(device)
         self.weights = weights or LlamaWeights(cfg, device=device, seed=seed)
         self.pool = KvPool(cfg, num_blocks, device)
-        self.runner = LlamaRunner(self.weights, self.pool)
+        self.runner = (runner_factory or LlamaRunner)(self.weights, self.pool)
+        self.token_vocab = token_vocab or cfg.vocab
         self.compute = torch.cuda.Stream(device=self.device)
         self.swapper = torch.cuda.Stream(device=self.device)
         self.swap_mode = swap_mode
@@ -120,7 +126,7 @@ class KvDataPath:
         keys, ids = [], []
         for req in workload:
             for seg in req.segments:
-                toks = segment_token_ids(req.id, seg.index, seg.n_in, self.cfg.vocab, self.token_seed)
+                toks = segment_token_ids(req.id, seg.index, seg.n_in, self.token_vocab, self.token_seed)
                 keys.append((req.id, seg.index, len(ids), len(toks)))
                 ids.extend(toks)
         buf = torch.tensor(ids or [0], dtype=torch.int32, device=self.device)
@@ -282,7 +288,7 @@ class KvDataPath:
             staged = self.staged.get((rid, m.segment_index))
             off = len(new_ids_host)
             if staged is None:
-                new_ids_host.extend(segment_token_ids(rid, m.segment_index, n_new, cfg.vocab, self.token_seed))
+                new_ids_host.extend(segment_token_ids(rid, m.segment_index, n_new, self.token_vocab, self.token_seed))
             plen = (ctx_before - start) + n_new
             plan.append(dict(rd=rd, start=start, plen=plen, new_off=off, n_new=n_new, n_gen=seg.n_gen,
                              ctx_before=ctx_before, recompute=recompute, staged=staged))

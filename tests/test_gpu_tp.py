@@ -41,3 +41,25 @@ def test_tensor_parallel_ranks_match_oracle(world, tmp_path):
             assert step["rel"] < 1e-2, step
     assert all(r == ranks[0] for r in ranks) or all(
         [s["token"] for s in r] == [s["token"] for s in ranks[0]] for r in ranks)
+
+
+def test_tensor_parallel_engine(tmp_path, golden):
+    """C5's deployment shape on the B200 kernels: two tensor-parallel ranks
+    (each holding half the heads, FFN and vocabulary, and only its kv-head
+    shard of the KV pool) execute every plan of the same reference schedule
+    -- prefill, decode, swaps, discards. Both ranks' reports equal the
+    reference's golden bytes, they generate identical tokens, and each
+    rank's pool holds half a token's KV."""
+    name = "c1b200/3600"
+    out = tmp_path / "tp_engine.json"
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    procs = [subprocess.Popen([sys.executable, str(HERE / "mp_gpu_tp_engine_worker.py"), str(r), "2", name,
+                               str(out)], env=env) for r in range(2)]
+    for p in procs:
+        assert p.wait(timeout=900) == 0
+    r0, r1 = json.loads(out.read_text())
+    assert r0["sha"] == r1["sha"] == golden[name]["sha256"]
+    assert r0["tokens"] == r1["tokens"]
+    assert r0["free"] and r1["free"] and r0["swap_outs"] > 0
+    from paper_2512_14142_b200.gpu.model import PRESETS
+    assert r0["kv_bytes_per_token"] * 2 == PRESETS["small"].kv_bytes_per_token
