@@ -231,11 +231,53 @@ struct TmaPages {
   int k_row0, v_row0;      // (layer, head) row offsets of the K and V pages within a block
 };
 
+// Issue the TMA of page k (of pages pa, pa + pstep, ...) into stage (cnt + k) % S.
+template <int D, int S>
+__device__ __forceinline__ void attn_tma_issue(const TmaPages& T, int k, int blk, uint8_t* ring, uint64_t* bars,
+                                               uint32_t cnt) {
+  constexpr int PB = tma_page_bytes<D>();
+  constexpr int HALF = kAttnBT * 128;
+  const uint32_t slot = (cnt + k) % S;
+  uint64_t* bb = bars + slot;
+  uint8_t* stw = ring + slot * PB;
+  const int kr = blk * T.block_rows + T.k_row0, vr = blk * T.block_rows + T.v_row0;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the warp's reads of the stage come first
+  mbar_arrive_expect_tx(bb, PB);
+#pragma unroll
+  for (int hf = 0; hf < D / 64; ++hf) {
+    tc::tma_load_2d(stw + hf * HALF, T.map, bb, hf * 64, kr);
+    tc::tma_load_2d(stw + (D / 64) * HALF + hf * HALF, T.map, bb, hf * 64, vr);
+  }
+}
+
+// Before the wait for the previous kernel: issue the first stages' pages
+// that hold only older tokens. In a decode step the previous kernel appends
+// just the newest token (position ctx - 1) of this layer; every kernel that
+// wrote older pages completed before the step began. Returns how many of the
+// first S pages were issued (a prefix); attn_pages_tma(pre = that) issues the rest.
+template <int D, int S>
+__device__ __forceinline__ int attn_pages_tma_preissue(const TmaPages& T, const int32_t* trow, int pa, int pb,
+                                                       int pstep, int ctx_b, uint8_t* ring, uint64_t* bars,
+                                                       uint32_t cnt, int lane) {
+  const int my = pb > pa ? (pb - pa + pstep - 1) / pstep : 0;
+  const int new_page = (ctx_b - 1) / kAttnBT;
+  int n = 0;
+  while (n < S && n < my && pa + pstep * n < new_page) ++n;
+  const int blk = lane < n ? __ldg(trow + pa + pstep * lane) : 0;
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    const int b = __shfl_sync(0xffffffffu, blk, k);
+    if (lane == 0 && k < n) attn_tma_issue<D, S>(T, k, b, ring, bars, cnt);
+  }
+  return n;
+}
+
 template <int D, int S>
 __device__ __forceinline__ void attn_pages_tma(const TmaPages& T, const int32_t* trow, int pa, int pb, int pstep,
                                                int ctx_b, float scale_log2, const uint32_t (*qa)[2],
                                                uint8_t* ring, uint64_t* bars, uint32_t& cnt, AttnAcc<D>& st,
-                                               int lane) {
+                                               int lane, int pre = 0) {
+  // pre: the first `pre` pages were issued already (attn_pages_tma_preissue)
   constexpr int PB = tma_page_bytes<D>();
   constexpr int HALF = kAttnBT * 128;
   constexpr int KS = D / 16, NT = D / 8;
@@ -249,23 +291,11 @@ __device__ __forceinline__ void attn_pages_tma(const TmaPages& T, const int32_t*
   if (my == 0) return;
   auto ids_of = [&](int w0) { return w0 + lane < my ? __ldg(trow + pa + pstep * (w0 + lane)) : 0; };
   int blk_c = ids_of(0), blk_n = ids_of(32);
-  auto issue = [&](int k, int blk) {   // lane 0: page k into stage (cnt + k) % S
-    const uint32_t slot = (cnt + k) % S;
-    uint64_t* bb = bars + slot;
-    uint8_t* stw = ring + slot * PB;
-    const int kr = blk * T.block_rows + T.k_row0, vr = blk * T.block_rows + T.v_row0;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the warp's reads of the stage come first
-    mbar_arrive_expect_tx(bb, PB);
-#pragma unroll
-    for (int hf = 0; hf < D / 64; ++hf) {
-      tc::tma_load_2d(stw + hf * HALF, T.map, bb, hf * 64, kr);
-      tc::tma_load_2d(stw + (D / 64) * HALF + hf * HALF, T.map, bb, hf * 64, vr);
-    }
-  };
+  auto issue = [&](int k, int blk) { attn_tma_issue<D, S>(T, k, blk, ring, bars, cnt); };   // lane 0
 #pragma unroll
   for (int k = 0; k < S; ++k) {
     const int blk = __shfl_sync(0xffffffffu, blk_c, k);
-    if (lane == 0 && k < my) issue(k, blk);
+    if (lane == 0 && k < my && k >= pre) issue(k, blk);
   }
   const int quad = lane & 3;
   for (int k = 0; k < my; ++k) {
@@ -544,23 +574,30 @@ __device__ __forceinline__ void attn_cta_phase(const AttnWork& A, int cta, int g
   AttnPiece pc;
   while (sp.next(pc)) {
     const int b = pc.b, h = pc.h;
+    const int ctx_b = __ldg(A.ctx + b);   // the step's contexts and tables: ready before any wait
+    int pre = 0;
+    TmaPages T;
+    if constexpr (AS > 1) {
+      T = *tp;
+      T.k_row0 = (A.layer * 2 * A.Hkv + h) * kAttnBT;
+      T.v_row0 = T.k_row0 + A.Hkv * kAttnBT;
+      // pages of older tokens stream while the previous kernel finishes
+      pre = attn_pages_tma_preissue<D, AS>(T, A.table + (long long)b * A.max_blocks, pc.pa + warp, pc.pb, 4,
+                                           ctx_b, reinterpret_cast<uint8_t*>(vs), abar + warp * AS, *acnt, lane);
+    }
     if (!(heads_ready >> h & 1)) {
       wait_head(h, lane);
       heads_ready |= 1u << h;
     }
     mark(1);
-    const int ctx_b = __ldg(A.ctx + b);
     const int r8 = lane >> 2, quad = lane & 3;
     AttnAcc<D> st;
     if constexpr (AS > 1) {
       uint32_t qs[D / 16][2];
       attn_load_q_std<D>(A.q + (long long)b * A.q_stride + (long long)(h * G + r8) * D, r8 < G, quad, qs);
       mark(2);
-      TmaPages T = *tp;
-      T.k_row0 = (A.layer * 2 * A.Hkv + h) * kAttnBT;
-      T.v_row0 = T.k_row0 + A.Hkv * kAttnBT;
       attn_pages_tma<D, AS>(T, A.table + (long long)b * A.max_blocks, pc.pa + warp, pc.pb, 4, ctx_b, A.scale_log2,
-                            qs, reinterpret_cast<uint8_t*>(vs), abar + warp * AS, *acnt, st, lane);
+                            qs, reinterpret_cast<uint8_t*>(vs), abar + warp * AS, *acnt, st, lane, pre);
     } else {
       uint32_t qa[D / 8];
       attn_load_q<D>(A.q + (long long)b * A.q_stride + (long long)(h * G + r8) * D, r8 < G, quad, qa);
