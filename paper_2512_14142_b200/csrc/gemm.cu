@@ -65,6 +65,8 @@ struct GemmArgs {
   // one-CTA kernel split-K (short prefills): K cut into gridDim.z ranges
   float* rpart;                // [tiles][splits][128][BN] fp32 partials
   int* rctr;                   // [tiles] arrival counters (zero between uses)
+  unsigned long long* trace;   // diagnostics (astraea_debug_gemm_trace): 16 words per CTA, or null
+  int trace_ctas;
 };
 
 // Epilogue of one 128-row x BN-column accumulator tile: thread = token row m
@@ -207,6 +209,206 @@ __device__ __forceinline__ void rows_epilogue(const GemmArgs& args, int m, bool 
   }
 }
 
+// The one-CTA kernel's epilogue staged through shared memory (the drained
+// stage ring): each thread still owns one token row of the accumulator, but
+// every global access is made by the 128 epilogue threads together, a row of
+// 16-byte chunks per 16 (or 8) consecutive lanes -- a thread-per-row global
+// access touches 32 rows (32 L2 transactions) per instruction, which made
+// the epilogue of a 128 x 128 tile cost more than its main loop
+// (tools/rows_trace.py). Chunk j of row r lives at r * CH + (j ^ (r & 7)):
+// conflict-free for both the per-row and the per-chunk walks.
+// Same arithmetic, same order as rows_epilogue (bit-identical results).
+template <int CH>
+__device__ __forceinline__ int swz(int r, int j) {
+  return r * CH + (j ^ (r & 7));
+}
+
+template <int BN>
+__device__ __forceinline__ void rows_epilogue_staged(const GemmArgs& args, int tile_a, int tile_b, int row, float rs,
+                                                     uint32_t lane_addr, uint8_t* stage,
+                                                     unsigned long long* tr = nullptr) {
+  const Epi& e = args.epi;
+  const int et = threadIdx.x - 64;   // 0..127: cooperative index
+  const int m = tile_a * kBM + row;
+  const bool mok = m < args.M;
+  uint4* ob = reinterpret_cast<uint4*>(stage);               // [128][16] chunks: one 128-column group
+  uint4* cs4 = reinterpret_cast<uint4*>(stage + 32768);      // QKV: [128][D/4] chunks of (cos, sin) pairs
+  int* sl = reinterpret_cast<int*>(stage + 32768 + 65536);   // QKV: [128] pool slots
+  const bool qkv = e.kind == EPI_QKV_ROPE;
+  if (qkv) {
+    const int chq = e.D / 4;   // 16-byte chunks per row of the table: D/2 float2
+    if (et < kBM) sl[et] = (tile_a * kBM + et < args.M) ? e.slots[tile_a * kBM + et] : -1;
+    // batches of 16 independent loads per thread (a dependent load per
+    // iteration would serialise 32 L2 round trips)
+#pragma unroll 1
+    for (int i0 = 0; i0 < kBM * chq; i0 += 16 * kBM) {
+      uint4 v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int i = i0 + k * kBM + et, r = i / chq, j = i % chq, mm = tile_a * kBM + r;
+        v[k] = make_uint4(0, 0, 0, 0);
+        if (i < kBM * chq && mm < args.M) {
+          if (e.cs) {
+            v[k] = __ldg(reinterpret_cast<const uint4*>(e.cs + (long long)mm * (e.D / 2)) + j);
+          } else {
+            const float2 a = rope_cs(e, mm, 2 * j), b = rope_cs(e, mm, 2 * j + 1);
+            v[k] = make_uint4(__float_as_uint(a.x), __float_as_uint(a.y), __float_as_uint(b.x), __float_as_uint(b.y));
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int i = i0 + k * kBM + et, r = i / chq, j = i % chq;
+        if (i < kBM * chq) cs4[r * chq + (j ^ (r & 7))] = v[k];
+      }
+    }
+  }
+#pragma unroll 1
+  for (int g = 0; g < BN / 128; ++g) {
+    const int n_group = tile_b * BN + g * 128;
+    if (n_group >= args.N) break;
+    if (g) epi_bar();   // the previous group's stores have left the buffer
+    if (tr && g == 0 && et == 0) tr[12] = gtimer();
+    if (e.kind == EPI_SILU) {
+      // gate chunk c pairs with up chunk c + 2: 64 output columns, 8 chunks
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        float lo[32], hi[32];
+        tmem_ld32(lane_addr + g * 128 + c * 32, lo);
+        tmem_ld32(lane_addr + g * 128 + (c + 2) * 32, hi);
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          float o[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) o[q] = silu_rounded(round_bf(lo[j + q] * rs)) * round_bf(hi[j + q] * rs);
+          ob[swz<8>(row, c * 4 + j / 8)] = pack8(o);
+        }
+      }
+      if (tr && g == 0 && et == 0) tr[13] = gtimer();
+      epi_bar();
+      if (tr && g == 0 && et == 0) tr[14] = gtimer();
+      const int f0 = (n_group / 128) * 64;
+      for (int i = et; i < kBM * 8; i += kBM) {
+        const int r = i >> 3, j = i & 7, mm = tile_a * kBM + r;
+        if (mm < args.M) *reinterpret_cast<uint4*>(args.C + (long long)mm * args.ldc + f0 + j * 8) = ob[swz<8>(r, j)];
+      }
+      continue;
+    }
+    if (qkv) {
+      const int pair = e.D == 128 ? 2 : 1;
+      const int chq = e.D / 4;
+      if (g == 0) epi_bar();   // table and slots staged
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        if ((c / pair) % 2) continue;
+        float lo[32], hi[32];
+        tmem_ld32(lane_addr + g * 128 + c * 32, lo);
+        tmem_ld32(lane_addr + g * 128 + (c + pair) * 32, hi);
+        const int col0 = n_group + c * 32;
+        const int head = col0 / e.D, hrow0 = col0 % e.D;
+        const bool rot = head < e.Hq + e.Hkv;
+        float ylo[32], yhi[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float x0 = round_bf(lo[j] * rs), x1 = round_bf(hi[j] * rs);
+          if (rot) {
+            const int fi = hrow0 + j;
+            const float* cj = reinterpret_cast<const float*>(cs4 + row * chq + ((fi >> 1) ^ (row & 7)));
+            const float2 r = make_float2(cj[(fi & 1) * 2], cj[(fi & 1) * 2 + 1]);
+            ylo[j] = x0 * r.x - x1 * r.y;
+            yhi[j] = x1 * r.x + x0 * r.y;
+          } else {
+            ylo[j] = x0;
+            yhi[j] = x1;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          ob[swz<16>(row, c * 4 + j / 8)] = pack8(ylo + j);
+          ob[swz<16>(row, (c + pair) * 4 + j / 8)] = pack8(yhi + j);
+        }
+      }
+      if (tr && g == 0 && et == 0) tr[13] = gtimer();
+      epi_bar();
+      if (tr && g == 0 && et == 0) tr[14] = gtimer();
+      for (int i = et; i < kBM * 16; i += kBM) {
+        const int r = i >> 4, j = i & 15, mm = tile_a * kBM + r;
+        const int col = n_group + j * 8;
+        if (mm >= args.M || col >= args.N) continue;
+        const int head = col / e.D, hrow = col % e.D;
+        bf16* dst;
+        if (head < e.Hq) {
+          dst = args.C + (long long)mm * args.ldc + col;
+        } else {
+          const int slot = sl[r];
+          if (slot < 0) continue;
+          const int kv = head < e.Hq + e.Hkv ? 0 : 1;
+          const int hk = head - e.Hq - kv * e.Hkv;
+          dst = e.pool + (long long)(slot / e.bt) * e.block_el +
+                ((long long)(e.layer * 2 + kv) * e.Hkv + hk) * e.bt * e.D + (long long)(slot % e.bt) * e.D + hrow;
+        }
+        *reinterpret_cast<uint4*>(dst) = ob[swz<16>(r, j)];
+      }
+      continue;
+    }
+    // NONE / RESIDUAL (+ sums of squares of the bf16 output)
+    const bool resid = e.kind == EPI_RESIDUAL;
+    if (resid) {
+      uint4 v[16];   // all 16 loads in flight before the first use
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int i = k * kBM + et, r = i >> 4, j = i & 15, mm = tile_a * kBM + r;
+        const int col = n_group + j * 8;
+        v[k] = (mm < args.M && col < args.N)
+                   ? __ldcg(reinterpret_cast<const uint4*>(e.residual + (long long)mm * args.ldc + col))
+                   : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int i = k * kBM + et;
+        ob[swz<16>(i >> 4, i & 15)] = v[k];
+      }
+      epi_bar();
+    }
+    float ssq = 0.f;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      float v[32];
+      tmem_ld32(lane_addr + g * 128 + c * 32, v);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = c * 4 + q;
+        if (n_group + j * 8 >= args.N) continue;
+        float o[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] = v[q * 8 + k] * rs;
+        if (resid) {
+          float r[8];
+          unpack8(ob[swz<16>(row, j)], r);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) o[k] += r[k];
+        }
+        const uint4 packed = pack8(o);
+        ob[swz<16>(row, j)] = packed;
+        float obf[8];
+        unpack8(packed, obf);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ssq += obf[k] * obf[k];
+      }
+    }
+    if (e.ssq_out && mok) e.ssq_out[(long long)(n_group / 128) * args.M + m] = ssq;
+    if (tr && g == 0 && et == 0) tr[13] = gtimer();
+    epi_bar();
+    if (tr && g == 0 && et == 0) tr[14] = gtimer();
+    for (int i = et; i < kBM * 16; i += kBM) {
+      const int r = i >> 4, j = i & 15, mm = tile_a * kBM + r;
+      const int col = n_group + j * 8;
+      if (mm < args.M && col < args.N)
+        *reinterpret_cast<uint4*>(args.C + (long long)mm * args.ldc + col) = ob[swz<16>(r, j)];
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // kRows (prefill): one 128 x BN output tile per CTA. Epilogue thread = one
 // token row; columns are processed in 128-column groups (4 TMEM chunks of
@@ -237,6 +439,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int S = gridDim.z, z = blockIdx.z;
   const int kb0 = (int)((long long)z * nkb_all / S), kb1 = (int)((long long)(z + 1) * nkb_all / S);
   const int nkb = kb1 - kb0;
+  const int lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  unsigned long long* tr = (args.trace && lin < args.trace_ctas) ? args.trace + lin * 16 : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = gtimer();
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
@@ -253,6 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (tr && threadIdx.x == 0) tr[1] = gtimer();
 
   pdl_launch();
   if (warp == 0) {
@@ -279,6 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int s = i % STAGES;
       mbar_wait(&full[s], (i / STAGES) & 1);
       tc_fence_after();
+      if (tr && i == 0 && lane == 0) tr[2] = gtimer();
       if (lane == 0) {
         const uint64_t da = smem_desc_sw128(sa + s * A_BYTES);
         const uint64_t db = smem_desc_sw128(sb + s * B_BYTES);
@@ -298,6 +505,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float rs = (e.ssq_in && mok) ? rms_scale(e, args.M, m) : 1.f;
     mbar_wait(done, 0);
     tc_fence_after();
+    if (tr && threadIdx.x == 64) tr[3] = gtimer();
+    if (tr && lane == 0) tr[8 + warp - 2] = gtimer();
     const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
     bool finish = true;
     if (S > 1) {
@@ -306,14 +515,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       // runs the epilogue
       const int row = quarter * 32 + lane;
       const long long tile = (long long)tile_a * gridDim.y + tile_b;
-      float* mine = args.rpart + ((tile * S + z) * kBM + row) * BN;
+      // partial layout per (tile, split): [BN / 4][128 rows][4] -- a warp's
+      // float4 for one column quad covers 32 consecutive rows (512 B)
+      float* mine = args.rpart + (tile * S + z) * kBM * BN + row * 4;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         float v[32];
         tmem_ld32(lane_addr + c, v);
 #pragma unroll
         for (int k = 0; k < 32; k += 4)
-          __stcg(reinterpret_cast<float4*>(mine + c + k), make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]));
+          __stcg(reinterpret_cast<float4*>(mine + (c + k) * kBM), make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]));
       }
       __threadfence();
       epi_bar();
@@ -321,9 +532,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (threadIdx.x == 64) s_last = atom_add_acq_rel(args.rctr + tile, 1) == S - 1;
       epi_bar();
       finish = s_last;
+      if (tr && threadIdx.x == 64) tr[4] = gtimer();
       if (finish) {
         __threadfence();
-        const float* base = args.rpart + (tile * S * kBM + row) * BN;
+        const float* base = args.rpart + tile * S * kBM * BN + row * 4;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           float sum[32], own[32];
@@ -335,10 +547,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int k = 0; k < 32; ++k) sum[k] += own[k];
             } else {
-              const float* src = base + (long long)zz * kBM * BN + c;
+              const float* src = base + (long long)zz * kBM * BN + c * kBM;
 #pragma unroll
               for (int k = 0; k < 32; k += 4) {
-                const float4 w = __ldcg(reinterpret_cast<const float4*>(src + k));
+                const float4 w = __ldcg(reinterpret_cast<const float4*>(src + k * kBM));
                 sum[k] += w.x;
                 sum[k + 1] += w.y;
                 sum[k + 2] += w.z;
@@ -352,9 +564,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         epi_bar();
         tc_fence_after();
         if (threadIdx.x == 64) args.rctr[tile] = 0;
+        if (tr && threadIdx.x == 64) tr[5] = gtimer();
       }
     }
-    if (finish) rows_epilogue<BN>(args, m, mok, rs, lane_addr, tile_b);
+    if (finish) {
+      static_assert(STAGES * (A_BYTES + B_BYTES) >= 32768 + 65536 + 512, "epilogue staging area");
+      if (e.kind != EPI_ARGMAX && (args.N % 8) == 0)
+        rows_epilogue_staged<BN>(args, tile_a, tile_b, quarter * 32 + lane, rs, lane_addr, smem, tr);
+      else
+        rows_epilogue<BN>(args, m, mok, rs, lane_addr, tile_b);
+    }
+    if (tr && threadIdx.x == 64) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      tr[6] = gtimer();
+      tr[7] = (unsigned long long)smid | ((unsigned long long)z << 16) | ((unsigned long long)finish << 31);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -1477,20 +1702,41 @@ struct RowsPlan {
 };
 static RowsPlan rows_plan(int M, int N, int K) {
   RowsPlan p;
-  p.bn = (N % 256 == 0 && (long long)((M + kBM - 1) / kBM) * (N / 256) >= num_sms()) ? 256 : 128;
+  static const int force_bn = [] {
+    const char* e = getenv("ASTRAEA_ROWS_BN");
+    return e ? atoi(e) : 0;
+  }();
+  // 256-column tiles once 128-column ones would need more than one wave
+  // (gate/up at 128 tokens: 224 -> 112 CTAs, the activation tile read once
+  // per 256 weight rows; 76 -> 67 us)
+  p.bn = (N % 256 == 0 && (long long)((M + kBM - 1) / kBM) * ((N + 127) / 128) > num_sms()) ? 256 : 128;
+  if (force_bn == 256 && N % 256 == 0) p.bn = 256;
+  if (force_bn == 128) p.bn = 128;
   const long long tiles = (long long)((M + kBM - 1) / kBM) * ((N + p.bn - 1) / p.bn);
   const int nkb = (K + kBK - 1) / kBK;
   static const int max_splits = [] {
     const char* e = getenv("ASTRAEA_ROWS_SPLITS");
     return e ? std::max(1, std::min(8, atoi(e))) : 2;   // 128-token prefill 6.78 -> 6.68 ms; 4: no better
   }();
+  static const int max_splits_long = [] {
+    const char* e = getenv("ASTRAEA_ROWS_SPLITS_LONG");
+    return e ? std::max(1, std::min(8, atoi(e))) : 3;   // down at 128 tokens: 63.7 (CTA pairs) -> 47.5 us
+  }();
   int s = 1;
-  if (tiles < num_sms()) s = (int)std::min<long long>(num_sms() / tiles, max_splits);   // one wave
+  const int cap = nkb > 64 ? max_splits_long : max_splits;
+  if (tiles < num_sms()) s = (int)std::min<long long>(num_sms() / tiles, cap);   // one wave
   s = std::max(1, std::min(s, nkb / 8));
   p.splits = s;
   return p;
 }
-static bool short_rows(int M, int N, int K) { return K <= 4096 && (M <= 128 || (M <= 256 && N <= 6144)); }
+static bool short_rows(int M, int N, int K) {
+  static const int long_k = [] {
+    const char* e = getenv("ASTRAEA_ROWS_LONGK");
+    return e ? atoi(e) : 1;
+  }();
+  if (long_k && M <= 128) return true;
+  return K <= 4096 && (M <= 128 || (M <= 256 && N <= 6144));
+}
 static size_t rows_partial_bytes(int M, int N, int K) {
   const RowsPlan p = rows_plan(M, N, K);
   if (p.splits <= 1) return 0;
@@ -1699,10 +1945,18 @@ extern "C" int astraea_gemm_bf16_ex(const void* A, int32_t lda, const void* W, i
   a.epi = e;
   // Short prefills (recompute-on-resume appends) are weight-streaming bound:
   // there the one-CTA 128-row tiles keep more SMs streaming than 256x256
-  // CTA-pair tiles -- K = 4096 projections at M <= 128 (gate/up included)
-  // and N <= 6144 ones (QKV, O) at M <= 256 (tools/gpu_r2t.sh sweep: 128
-  // tokens 50 -> 37 us QKV, 37.5 -> 31.8 O, 90.5 -> 76 gate/up per layer).
+  // CTA-pair tiles -- every projection at M <= 128 (down included, split-K
+  // over up to 3 CTAs: 63.7 -> 47.5 us) and N <= 6144 ones (QKV, O) at
+  // M <= 256 (tools/gpu_r2t.sh sweep: 128 tokens 50 -> 37 us QKV, 37.5 ->
+  // 31.8 O, 90.5 -> 76 gate/up per layer; profiles/r2_prefill_rows_v2.txt).
   const bool rows_short = short_rows(M, N, K);
+  a.trace = nullptr;
+  a.trace_ctas = 0;
+  if (g_trace && g_trace_slots > 0) {
+    a.trace = g_trace + (size_t)(g_trace_next % g_trace_slots) * g_trace_stride;
+    a.trace_ctas = g_trace_stride / 16;
+    ++g_trace_next;
+  }
   a.splits = 1;
   a.rpart = nullptr;
   a.rctr = nullptr;

@@ -100,8 +100,10 @@ __host__ __device__ constexpr uint32_t instr_desc(int n) {
 __device__ __forceinline__ float round_bf(float x) { return bf2f(f2bf(x)); }
 
 __device__ __forceinline__ float silu_rounded(float g) {
-  // silu(g) is materialised in bf16 by the reference formulation
-  return round_bf(g / (1.f + __expf(-g)));
+  // silu(g) is materialised in bf16 by the reference formulation. Fast
+  // division: an IEEE divide takes its slow path whenever exp(-g)
+  // overflows (g < -88), ~100 instructions per element.
+  return round_bf(__fdividef(g, 1.f + __expf(-g)));
 }
 
 // ---- epilogue program --------------------------------------------------------------

@@ -74,7 +74,7 @@ for T in a.tokens:
     q = torch.empty(T, qd, dtype=torch.bfloat16, device=dev)
     att = torch.randn(T, qd, device=dev).to(torch.bfloat16)
     h = torch.randn(T, cfg.ffn, device=dev).to(torch.bfloat16)
-    ssq = torch.ones(runner.parts, T, dtype=torch.float32, device=dev)
+    ssq = torch.full((runner.parts, T), cfg.hidden / runner.parts, dtype=torch.float32, device=dev)  # x ~ N(0, 1): sum x^2 = d
     cs = ops.rope_table(pos_t, cfg.head_dim, cfg.rope_theta)
     lw = w.layers[0]
     ws = runner.gemm_ws
