@@ -60,7 +60,7 @@ def calibrate(dp, prefill_points=(128, 256, 512, 1024, 2048), decode_batches=(1,
         slots = d([blocks[p // 16] * 16 + p % 16 for p in range(n)])
         table = d([blocks]).view(1, -1)
         args = (ids, pos, slots, d([0, n]), table, d([n]), torch.tensor([n - 1], device=dev), n)
-        prefill.append([n, _time(lambda: runner.prefill(*args), reps)])
+        prefill.append([n, _time(lambda: runner.prefill(*args), max(reps, 5), warm=2)])
     decode = {}
     nb = (decode_ctx + 16) // 16
     for B in decode_batches:
@@ -70,7 +70,19 @@ def calibrate(dp, prefill_points=(128, 256, 512, 1024, 2048), decode_batches=(1,
         slots = table[:, decode_ctx // 16] * 16 + decode_ctx % 16
         ctx = torch.full((B,), decode_ctx + 1, dtype=torch.int32, device=dev)
         keys = torch.zeros(B, dtype=torch.int64, device=dev)
-        decode[B] = _time(lambda: runner.decode(tok, pos, slots, table, ctx, keys_out=keys), reps)
+        # the data path replays decode steps from CUDA graphs: time a graph
+        # replay (an eager call also times the host launching ~35 kernels)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                runner.decode(tok, pos, slots, table, ctx, stream=side, keys_out=keys)
+        torch.cuda.current_stream().wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=side):
+            runner.decode(tok, pos, slots, table, ctx, stream=side, keys_out=keys)
+        decode[B] = _time(graph.replay, max(reps, 10), warm=3)
+        del graph
     ids = list(range((swap_tokens + 15) // 16))
     slot = torch.empty(swap_tokens * pool.bytes_per_token, dtype=torch.uint8, pin_memory=True)
     t_out = _time(lambda: ops.swap_out(pool.geo, pool.data, ids, swap_tokens, slot, dp.swap_mode), reps)

@@ -92,3 +92,18 @@ def test_8b_engine_c2_report_matches_reference(name, golden, w8b):
     assert dev["swap_outs"] == decisions.get("swap:estimated", 0)
     assert dev["discards"] == decisions.get("discard:estimated", 0) + decisions.get("discard:deadlock-evicted", 0)
     assert PRESETS["llama3-8b"].kv_bytes_per_token == 131072
+
+
+def test_calibration_tables_load_into_the_reference_predictor():
+    """gpu/calibrate.py on the tiny model: every table entry is a positive
+    device time, decode is timed from a CUDA graph replay, and the tables load
+    into the reference's ServiceTimePredictor (predictor.py:47-66)."""
+    from paper_2512_14142_b200.gpu import calibrate
+    dp = datapath_for(4096, model="tiny")
+    cal = calibrate.calibrate(dp, prefill_points=(32, 64), decode_batches=(1, 2), decode_ctx=48, swap_tokens=64)
+    assert all(t > 0 for _, t in cal["predictor"]["prefill_profile"])
+    assert set(cal["decode_step_seconds_by_batch"]) == {"1", "2"}
+    assert all(v > 0 for v in cal["decode_step_seconds_by_batch"].values())
+    assert cal["swap_bandwidth_tokens_per_s"] > 0 and cal["swap"]["mode"] == "staged"
+    pred = calibrate.predictor_from_calibration(host, cal)
+    assert pred.to_config()["prefill_profile"][0][0] == 32
