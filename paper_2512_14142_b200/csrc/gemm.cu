@@ -232,17 +232,38 @@ __device__ __forceinline__ void rows_epilogue_staged(const GemmArgs& args, int t
   const int m = tile_a * kBM + row;
   const bool mok = m < args.M;
   uint4* ob = reinterpret_cast<uint4*>(stage);               // [128][16] chunks: one 128-column group
+  uint4* cs4 = reinterpret_cast<uint4*>(stage + 32768);      // QKV: [128][D/4] chunks of (cos, sin) pairs
   int* sl = reinterpret_cast<int*>(stage + 32768 + 65536);   // QKV: [128] pool slots
   const bool qkv = e.kind == EPI_QKV_ROPE;
-  // QKV: the rotation angles are recomputed per element, bit-identical to
-  // the table rope_table_kernel writes (same expression, IEEE sincosf /
-  // powf): cheaper than staging the 64 KB of (cos, sin) pairs of the tile's
-  // 128 tokens from L2 (6 us of the epilogue, tools/rows_trace.py)
-  float* invf = reinterpret_cast<float*>(stage + 32768);     // QKV: [D/2] inverse frequencies
-  const int pos_m = (qkv && mok) ? e.pos[m] : 0;
   if (qkv) {
+    const int chq = e.D / 4;   // 16-byte chunks per row of the table: D/2 float2
     if (et < kBM) sl[et] = (tile_a * kBM + et < args.M) ? e.slots[tile_a * kBM + et] : -1;
-    if (et < e.D / 2) invf[et] = 1.0f / powf(e.theta, (float)(2 * et) / (float)e.D);
+    // the (cos, sin) pairs of the tile's 128 tokens, staged with batches of
+    // 16 independent loads per thread (a dependent load per iteration would
+    // serialise 32 L2 round trips). Recomputing them per element instead
+    // (IEEE sincosf) measured slower: QKV 34.6 -> 36.1 us at 128 tokens.
+#pragma unroll 1
+    for (int i0 = 0; i0 < kBM * chq; i0 += 16 * kBM) {
+      uint4 v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int i = i0 + k * kBM + et, r = i / chq, j = i % chq, mm = tile_a * kBM + r;
+        v[k] = make_uint4(0, 0, 0, 0);
+        if (i < kBM * chq && mm < args.M) {
+          if (e.cs) {
+            v[k] = __ldg(reinterpret_cast<const uint4*>(e.cs + (long long)mm * (e.D / 2)) + j);
+          } else {
+            const float2 a = rope_cs(e, mm, 2 * j), b = rope_cs(e, mm, 2 * j + 1);
+            v[k] = make_uint4(__float_as_uint(a.x), __float_as_uint(a.y), __float_as_uint(b.x), __float_as_uint(b.y));
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int i = i0 + k * kBM + et, r = i / chq, j = i % chq;
+        if (i < kBM * chq) cs4[r * chq + (j ^ (r & 7))] = v[k];
+      }
+    }
   }
 #pragma unroll 1
   for (int g = 0; g < BN / 128; ++g) {
@@ -277,7 +298,8 @@ __device__ __forceinline__ void rows_epilogue_staged(const GemmArgs& args, int t
     }
     if (qkv) {
       const int pair = e.D == 128 ? 2 : 1;
-      if (g == 0) epi_bar();   // frequencies and slots staged
+      const int chq = e.D / 4;
+      if (g == 0) epi_bar();   // table and slots staged
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         if ((c / pair) % 2) continue;
@@ -292,10 +314,11 @@ __device__ __forceinline__ void rows_epilogue_staged(const GemmArgs& args, int t
         for (int j = 0; j < 32; ++j) {
           const float x0 = round_bf(lo[j] * rs), x1 = round_bf(hi[j] * rs);
           if (rot) {
-            float sn, cs;
-            sincosf((float)pos_m * invf[hrow0 + j], &sn, &cs);
-            ylo[j] = x0 * cs - x1 * sn;
-            yhi[j] = x1 * cs + x0 * sn;
+            const int fi = hrow0 + j;
+            const float* cj = reinterpret_cast<const float*>(cs4 + row * chq + ((fi >> 1) ^ (row & 7)));
+            const float2 r = make_float2(cj[(fi & 1) * 2], cj[(fi & 1) * 2 + 1]);
+            ylo[j] = x0 * r.x - x1 * r.y;
+            yhi[j] = x1 * r.x + x0 * r.y;
           } else {
             ylo[j] = x0;
             yhi[j] = x1;
