@@ -207,7 +207,7 @@ def test_prefill_attention(Hq, Hkv, D, lens_ctx):
 @pytest.mark.parametrize("M,N,K", [(1, 4096, 4096), (3, 6144, 4096), (16, 512, 512), (17, 1536, 512),
                                    (32, 28672, 4096), (64, 4096, 14336), (65, 4096, 4096), (128, 256, 64),
                                    (300, 6144, 4096), (513, 1024, 512), (2048, 4096, 4096), (129, 32000, 512),
-                                   (7, 128256, 4096)])
+                                   (7, 128256, 4096), (100, 1000, 512), (90, 4104, 14336), (128, 28672, 4096)])
 def test_gemm_matches_fp32(M, N, K):
     g = torch.Generator(device=DEV).manual_seed(M * 7 + N)
     a = (torch.randn(M, K, generator=g, device=DEV)).bfloat16()
@@ -218,7 +218,7 @@ def test_gemm_matches_fp32(M, N, K):
     assert rel_err(out, ref) < 5e-3
 
 
-@pytest.mark.parametrize("M", [4, 200])
+@pytest.mark.parametrize("M", [4, 100, 200])
 def test_gemm_residual_in_place(M):
     N, K = 1024, 2048
     g = torch.Generator(device=DEV).manual_seed(5)
@@ -349,7 +349,7 @@ def _rms_parts(x, parts):
     return torch.stack([xf[:, p * 128:(p + 1) * 128].pow(2).sum(-1) for p in range(parts)])
 
 
-@pytest.mark.parametrize("M", [3, 17, 64, 200])
+@pytest.mark.parametrize("M", [3, 17, 64, 100, 200])
 def test_gemm_residual_emits_norm_statistics(M):
     N, K = 1024, 512
     g = torch.Generator(device=DEV).manual_seed(M)
@@ -364,9 +364,9 @@ def test_gemm_residual_emits_norm_statistics(M):
     assert rel_err(ssq, _rms_parts(x, N // 128)) < 1e-5   # statistics of the stored bf16 output
 
 
-@pytest.mark.parametrize("M", [1, 16, 40, 150])
-def test_gemm_rms_scaled_silu(M):
-    F, K = 1536, 512
+@pytest.mark.parametrize("M,F", [(1, 1536), (16, 1536), (40, 1536), (100, 1536), (150, 1536), (100, 14336)])
+def test_gemm_rms_scaled_silu(M, F):
+    K = 512
     g = torch.Generator(device=DEV).manual_seed(7 + M)
     x = torch.randn(M, K, generator=g, device=DEV).bfloat16()
     wgu = (torch.randn(2 * F, K, generator=g, device=DEV) * 0.05).bfloat16()
@@ -382,7 +382,7 @@ def test_gemm_rms_scaled_silu(M):
     assert rel_err(out, ref) < 1e-2
 
 
-@pytest.mark.parametrize("M", [2, 33, 130])
+@pytest.mark.parametrize("M", [2, 33, 100, 130])
 @pytest.mark.parametrize("Hq,Hkv,D", [(32, 8, 128), (8, 2, 64)])
 def test_gemm_qkv_rope_append(M, Hq, Hkv, D):
     K, Lyr, nb = 512, 2, 40
@@ -528,7 +528,7 @@ def test_fused_chain_attention_matches_oracle(Hq, Hkv, D, ctxs):
         assert torch.equal(y, y_ref), rep
 
 
-@pytest.mark.parametrize("M,N", [(100, 4096), (128, 6144), (200, 4096)])
+@pytest.mark.parametrize("M,N", [(100, 4096), (128, 6144), (200, 4096), (97, 4104)])
 def test_short_prefill_split_k_rows(M, N):
     """Short prefills on the one-CTA kernel with split-K (tiles < SMs): fp32
     partials summed in split order by the last split -- matches fp32, is
