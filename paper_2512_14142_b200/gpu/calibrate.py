@@ -61,9 +61,17 @@ def calibrate(dp, prefill_points=(128, 256, 512, 1024, 2048), decode_batches=(1,
         table = d([blocks]).view(1, -1)
         args = (ids, pos, slots, d([0, n]), table, d([n]), torch.tensor([n - 1], device=dev), n)
         prefill.append([n, _time(lambda: runner.prefill(*args), max(reps, 5), warm=2)])
+    # the reference's PrefillProfile requires non-decreasing latencies
+    # (predictor.py:47-57): launch-bound small points can measure out of
+    # order within noise, so keep the running maximum
+    for i in range(1, len(prefill)):
+        prefill[i][1] = max(prefill[i][1], prefill[i - 1][1])
     decode = {}
     nb = (decode_ctx + 16) // 16
-    for B in decode_batches:
+    # two passes over the batch sizes, the faster kept: the first decode timed
+    # right after the prefill points runs while clocks recover from the
+    # tensor-heavy prefills (batch 1 read 3.40 ms in one pass, 3.15 in the next)
+    for B in list(decode_batches) * 2:
         table = torch.arange(B * nb, dtype=torch.int32, device=dev).view(B, nb)
         tok = torch.zeros(B, dtype=torch.int32, device=dev)
         pos = torch.full((B,), decode_ctx, dtype=torch.int32, device=dev)
@@ -81,7 +89,8 @@ def calibrate(dp, prefill_points=(128, 256, 512, 1024, 2048), decode_batches=(1,
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=side):
             runner.decode(tok, pos, slots, table, ctx, stream=side, keys_out=keys)
-        decode[B] = _time(graph.replay, max(reps, 10), warm=3)
+        t = _time(graph.replay, max(reps, 10), warm=3)
+        decode[B] = min(t, decode.get(B, t))
         del graph
     ids = list(range((swap_tokens + 15) // 16))
     slot = torch.empty(swap_tokens * pool.bytes_per_token, dtype=torch.uint8, pin_memory=True)

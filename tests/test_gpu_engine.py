@@ -101,7 +101,8 @@ def test_calibration_tables_load_into_the_reference_predictor():
     from paper_2512_14142_b200.gpu import calibrate
     dp = datapath_for(4096, model="tiny")
     cal = calibrate.calibrate(dp, prefill_points=(32, 64), decode_batches=(1, 2), decode_ctx=48, swap_tokens=64)
-    assert all(t > 0 for _, t in cal["predictor"]["prefill_profile"])
+    prof = cal["predictor"]["prefill_profile"]
+    assert all(t > 0 for _, t in prof) and all(a[1] <= b[1] for a, b in zip(prof, prof[1:]))
     assert set(cal["decode_step_seconds_by_batch"]) == {"1", "2"}
     assert all(v > 0 for v in cal["decode_step_seconds_by_batch"].values())
     assert cal["swap_bandwidth_tokens_per_s"] > 0 and cal["swap"]["mode"] == "staged"
