@@ -1744,8 +1744,12 @@ static bool short_rows(int M, int N, int K) {
     const char* e = getenv("ASTRAEA_ROWS_LONGK_M");
     return e ? atoi(e) : 256;   // down projection at 129-256 tokens: 63 -> 48 us (CTA pairs -> split-K rows)
   }();
+  static const int rows_m = [] {
+    const char* e = getenv("ASTRAEA_ROWS_M");
+    return e ? atoi(e) : 512;   // QKV / O at 257-512 tokens: 54 / 38 -> 40-51 / 28 us (one wave of 128-row tiles)
+  }();
   if (long_k && (M <= 128 || (M <= long_k_m && N <= 8192))) return true;
-  return K <= 4096 && (M <= 128 || (M <= 256 && N <= 6144));
+  return K <= 4096 && (M <= 128 || (M <= rows_m && N <= 6144));
 }
 static size_t rows_partial_bytes(int M, int N, int K) {
   const RowsPlan p = rows_plan(M, N, K);
@@ -1957,7 +1961,7 @@ extern "C" int astraea_gemm_bf16_ex(const void* A, int32_t lda, const void* W, i
   // there the one-CTA 128-row tiles keep more SMs streaming than 256x256
   // CTA-pair tiles -- every projection at M <= 128 (down included, split-K
   // over up to 3 CTAs: 63.7 -> 47.5 us), N <= 8192 ones at M <= 256 (down:
-  // 63 -> 48 us) and N <= 6144 ones (QKV, O) at M <= 256 (tools/gpu_r2t.sh sweep: 128 tokens 50 -> 37 us QKV, 37.5 ->
+  // 63 -> 48 us) and N <= 6144 ones (QKV, O) at M <= 512 (tools/gpu_r2t.sh sweep: 128 tokens 50 -> 37 us QKV, 37.5 ->
   // 31.8 O, 90.5 -> 76 gate/up per layer; profiles/r2_prefill_rows_v2.txt).
   const bool rows_short = short_rows(M, N, K);
   a.trace = nullptr;
