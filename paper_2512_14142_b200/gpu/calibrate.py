@@ -41,6 +41,16 @@ def _time(fn, reps=3, warm=1):
     return statistics.median(out)
 
 
+def monotone_profile(points):
+    """The reference's PrefillProfile requires non-decreasing latencies
+    (predictor.py:47-57): launch-bound small points can measure out of order
+    within noise, so keep the running maximum."""
+    out = [[int(n), float(t)] for n, t in points]
+    for i in range(1, len(out)):
+        out[i][1] = max(out[i][1], out[i - 1][1])
+    return out
+
+
 def calibrate(dp, prefill_points=(128, 256, 512, 1024, 2048), decode_batches=(1, 2, 4, 8, 16), decode_ctx=512,
               swap_tokens=1024, reps=3) -> dict:
     cfg, runner, pool = dp.cfg, dp.runner, dp.pool
@@ -61,11 +71,7 @@ def calibrate(dp, prefill_points=(128, 256, 512, 1024, 2048), decode_batches=(1,
         table = d([blocks]).view(1, -1)
         args = (ids, pos, slots, d([0, n]), table, d([n]), torch.tensor([n - 1], device=dev), n)
         prefill.append([n, _time(lambda: runner.prefill(*args), max(reps, 5), warm=2)])
-    # the reference's PrefillProfile requires non-decreasing latencies
-    # (predictor.py:47-57): launch-bound small points can measure out of
-    # order within noise, so keep the running maximum
-    for i in range(1, len(prefill)):
-        prefill[i][1] = max(prefill[i][1], prefill[i - 1][1])
+    prefill = monotone_profile(prefill)
     decode = {}
     nb = (decode_ctx + 16) // 16
     # two passes over the batch sizes, the faster kept: the first decode timed

@@ -109,3 +109,20 @@ def test_report_with_device_audits_loads_in_the_reference():
     assert ref.RunReport.from_dict(d).to_json() == rep.to_json()
     table = ref.compare({"b200": back, "reference": scenarios.run_scenario(ref, name)}, baseline="reference")
     assert table is not None
+
+
+def test_calibrated_prefill_profile_is_valid_for_the_reference():
+    """Launch-bound prefill points can measure out of order; the calibration
+    keeps the running maximum so the reference's PrefillProfile (which
+    requires non-decreasing latencies, predictor.py:47-57) accepts them."""
+    from paper_2512_14142_b200.gpu import calibrate
+    raw = [[32, 3.4e-4], [64, 3.3e-4], [128, 5.7e-3], [256, 5.6e-3], [512, 9.0e-3]]
+    prof = calibrate.monotone_profile(raw)
+    assert [n for n, _ in prof] == [32, 64, 128, 256, 512]
+    assert all(a[1] <= b[1] for a, b in zip(prof, prof[1:]))
+    assert prof[1][1] == 3.4e-4 and prof[4][1] == 9.0e-3
+    cal = {"predictor": {"prefill_profile": prof, "decode_seconds_per_token": 3.1e-3, "api_latency_means": None}}
+    pred = calibrate.predictor_from_calibration(ref, cal)
+    assert pred.prefill_seconds(64) == pytest.approx(3.4e-4)
+    with pytest.raises(ref.ConfigError):
+        calibrate.predictor_from_calibration(ref, {"predictor": dict(cal["predictor"], prefill_profile=raw)})
