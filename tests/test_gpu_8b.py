@@ -76,7 +76,10 @@ def prefill(runner, seqs, tables):
 TOL_PREFILL = 1.25e-2
 
 
-@pytest.mark.parametrize("name,T", [("p512", 512), ("s1000", 1000)])
+# 100 tokens: every projection on the one-CTA kernel (staged epilogue, split-K
+# down, 256-column gate/up tiles); 200: QKV/O/down one-CTA, gate/up CTA pairs;
+# 512: QKV/O one-CTA, gate/up/down CTA pairs; 1000: all CTA pairs
+@pytest.mark.parametrize("name,T", [("p100", 100), ("p200", 200), ("p512", 512), ("s1000", 1000)])
 def test_8b_shape_prefill_logits(model, name, T):
     w, logical = model
     pool = KvPool(CFG, 80)
