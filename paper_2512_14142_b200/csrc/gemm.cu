@@ -1936,7 +1936,14 @@ extern "C" int astraea_gemm_bf16_ex(const void* A, int32_t lda, const void* W, i
   if (!C && e.kind != EPI_ARGMAX) return ASTRAEA_EINVAL;
   if (M == 0) return ASTRAEA_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  if (M <= kColsMaxM) {
+  static const int chain_max_m = [] {
+    const char* e = getenv("ASTRAEA_GEMM_CHAIN_MAX_M");
+    // a single GEMM of 33-64 rows (a short prefill) runs faster on the
+    // one-CTA kernel than on the BN = 64 stream-K kernel, whose epilogue
+    // loops over 64 tokens: 64-token prefill 8.33 -> 5.52 ms
+    return e ? std::min(kColsMaxM, std::max(1, atoi(e))) : 32;
+  }();
+  if (M <= chain_max_m) {
     astraea_gemm_phase ph;
     ph.A = A;
     ph.lda = lda;
